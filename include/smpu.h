@@ -1,0 +1,182 @@
+/*
+ * smpu.h -- Synchronous Mixed-Precision large-batch Update step: C ABI of libsmpu.so.
+ *
+ * The data-parallel hot path of Ott et al., "Scaling Neural Machine Translation"
+ * (arXiv 1806.00187), built B200-native (sm_100a).  One update step is
+ *
+ *   c x accumulate(micro_grads, ntokens)   fp16 gradient accumulation over `update_freq`
+ *                                          sub-batches ("cumul", PAPER.md 4.2 P:178, Table 1)
+ *   bucketed fp16 all-reduce, overlapped   "as soon as the size of the buffer reaches a predefined
+ *                                          threshold we synchronize" (PAPER.md 4.3 P:209-212, 150MB fn)
+ *   step()                                 overflow test, dynamic loss scaler, unscale and
+ *                                          normalise by the global target-token count,
+ *                                          fp32-master Adam 0.9/0.98/1e-8 with the
+ *                                          inverse-sqrt warmup LR, fp16 re-cast.
+ *
+ * Conventions for every call
+ *  - Pointers marked "device" are CUDA device pointers of the ctx's device; "host or device" pointers
+ *    are classified with cudaPointerGetAttributes (pinned or pageable host memory is accepted).
+ *  - `stream` arguments are cudaStream_t values passed as void*; NULL means the legacy default stream.
+ *    Reads of caller buffers are stream-ordered on that stream: the caller may reuse a buffer after
+ *    later work on the same stream.  Different calls may use different streams; the library orders its
+ *    own state across them with events.
+ *  - Every call returns smpu_status.  SMPU_EINVAL / SMPU_ESTATE leave the ctx unchanged (except where
+ *    stated).  SMPU_ECUDA / SMPU_ENCCL poison the ctx: every later call returns SMPU_EPOISONED.
+ *    smpu_last_error() gives a thread-local message for the last failing call.
+ *  - Non-finite gradients are NOT errors: they are the overflow signal the method reacts to.
+ *  - A ctx is not thread-safe.  All ranks of a world must make the same sequence of calls (NCCL).
+ *  - Arrays are packed in gradient-READY order (reverse forward order): tensor j occupies
+ *    elements [sum_{i<j} numel_i, sum_{i<=j} numel_i) of every per-parameter vector.  No padding.
+ */
+#ifndef SMPU_H
+#define SMPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMPU_ABI_VERSION 1
+#define SMPU_NCCL_ID_BYTES 128
+
+typedef struct smpu_ctx smpu_ctx;
+
+typedef enum {
+    SMPU_OK = 0,
+    SMPU_EINVAL = 1,     /* null / misaligned / out-of-range argument                                  */
+    SMPU_ESTATE = 2,     /* call-order violation (see smpu_step); also N = 0 at step (update discarded)   */
+    SMPU_ECUDA = 3,      /* CUDA runtime error: ctx poisoned                                            */
+    SMPU_ENCCL = 4,      /* NCCL error: ctx poisoned                                                    */
+    SMPU_ENOMEM = 5,     /* device or pinned-host allocation failed (init only)                         */
+    SMPU_EPOISONED = 6   /* an earlier call poisoned this ctx                                           */
+} smpu_status;
+
+typedef struct {
+    double peak_lr;            /* 5e-4; 1e-3 = "2x lr"                                  */
+    int64_t warmup_updates;    /* 4000                                                          */
+    double beta1, beta2, eps;  /* 0.9, 0.98, 1e-8                                               */
+    int32_t init_scale_log2;   /* 7: initial loss scale 2^7 (paper silent; reading R8)         */
+    int32_t min_scale_log2;    /* -5 (R8): halving stops here                                            */
+    int32_t max_scale_log2;    /* 24 (R8): growth stops here                                             */
+    int64_t growth_interval;   /* 2000 clean updates before the scale doubles                   */
+    int32_t update_freq;       /* c >= 1 micro-batches per update ("cumul")                      */
+    int64_t bucket_bytes;      /* 150 MiB of fp16 gradient per all-reduce bucket (P:212 footnote, R22)  */
+} smpu_config;
+
+typedef struct {
+    int32_t overflow;          /* 1 iff the reduced fp16 gradient held a non-finite element     */
+    int32_t applied;           /* 1 iff theta/m/v/w16 were updated (== !overflow unless discarded)       */
+    int32_t scale_log2_used;   /* e of the scale 2^e the micro-gradients of this update carried         */
+    int32_t scale_log2_next;   /* e after the scaler step: multiply the next losses by 2^this            */
+    float lr;                  /* fp32 lr(t) applied; on a skip, lr(t+1) (reading R15)                   */
+    int32_t discarded;         /* 1 iff global N was 0: nothing changed, the update is dropped (R19)     */
+    int64_t num_updates;       /* t after this call: applied updates only (reading R7)                   */
+    int64_t ntokens_total;     /* N: non-pad target tokens over all ranks and micro-batches       */
+    int64_t clean_streak;      /* consecutive clean updates since the last scale change                   */
+    int64_t attempt;           /* 1-based index of this update attempt (applied or not)                  */
+} smpu_step_result;
+
+/* which-selectors of smpu_get_state / smpu_set_state (checkpoint / resume, test access) */
+enum {
+    SMPU_STATE_MASTER = 0,     /* fp32[n] master weights theta                                           */
+    SMPU_STATE_M = 1,          /* fp32[n] Adam first moment                                               */
+    SMPU_STATE_V = 2,          /* fp32[n] Adam second moment                                              */
+    SMPU_STATE_W16 = 3,        /* fp16[n] model weights (the re-cast copy)                                */
+    SMPU_STATE_ACCUM = 4,      /* fp16[n] gradient accumulator (after step: the reduced gradient R)       */
+    SMPU_STATE_SCALARS = 5     /* int64[4] = {e, clean_streak, num_updates, attempts}                     */
+};
+
+/* kernel ids of smpu_kernel_stats */
+enum { SMPU_K1_FIRST = 0, SMPU_K1_ADD = 1, SMPU_K1S = 2, SMPU_K0 = 3, SMPU_K2 = 4, SMPU_KCAST = 5,
+       SMPU_NCCL_AR = 6, SMPU_N_KERNELS = 7 };
+
+int smpu_abi_version(void);
+
+/* Fill *cfg with the paper's defaults (values in the comments of smpu_config). */
+smpu_status smpu_config_default(smpu_config* cfg);
+
+/* NCCL unique id for world > 1: call on rank 0 only, distribute the SMPU_NCCL_ID_BYTES bytes to every
+ * rank out of band (the harness uses torch.distributed), pass to smpu_init.  `out` host, >= 128 B. */
+smpu_status smpu_unique_id(void* out, int64_t bytes);
+
+/* Host-only bucket plan (reading R17): walk the tensors in ready order, add whole tensors to
+ * the current bucket and close it as soon as its fp16 bytes reach bucket_bytes; the remainder is the
+ * last bucket.  bucket_begin (host, capacity n_tensors+1 entries, or NULL to query the count) receives
+ * the element offset of each bucket plus the total n at [*n_buckets].  Needs no GPU. */
+smpu_status smpu_plan_buckets(const int64_t* numel, int n_tensors, int64_t bucket_bytes, int* n_buckets,
+                              int64_t* bucket_begin);
+
+/* Create a ctx on CUDA device `cuda_device`.
+ *   cfg          host; copied.
+ *   world, rank  0 <= rank < world.  world > 1 needs nccl_id (host, 128 B, identical on every rank) and
+ *                every rank calling smpu_init concurrently (collective).
+ *   numel        host int64[n_tensors] > 0, gradient-ready order; copied.
+ *   init_params  host or device fp32[n]: theta_0; copied.  Rank 0's copy is broadcast so all replicas
+ *                start bitwise identical (P:55-57 synchronous data parallelism).
+ * Allocates theta, m, v (fp32), w16, accumulator (fp16) on the device: 16 B per parameter. */
+smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
+                      int cuda_device, const int64_t* numel, int n_tensors, const float* init_params);
+
+smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n);
+
+/* Bucket boundaries chosen at init (same as smpu_plan_buckets with cfg->bucket_bytes). */
+smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_begin /* or NULL */);
+
+/* Device fp16[n] weights (library-owned, valid until smpu_destroy).  Rewritten only by smpu_step,
+ * in stream order on the stream passed to it. */
+smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16);
+
+/* Device fp32 scalar holding the current loss scale 2^e ("we scale the loss right after the forward
+ * pass").  Updated in stream order by smpu_step; a producer multiplies its loss by it without a
+ * host round trip. */
+smpu_status smpu_loss_scale(const smpu_ctx* ctx, const float** dev_scale);
+
+/* One whole micro-batch.  micro_grads: host or device fp16[n] (bit patterns), packed; device buffers
+ * should be 32-byte aligned for the vector path (any 2-byte alignment is correct).  Gradients are those
+ * of the SCALED token-SUM loss of the micro-batch (reading R11).  ntokens >= 0: its non-pad target
+ * tokens.  Micro-batch 1 of an update copies, 2..c add in fp16 round-to-nearest-even (R1, R2).
+ * On the last micro-batch with world > 1 each bucket's all-reduce starts as soon as that bucket is
+ * accumulated.  ESTATE if c micro-batches were already given or a bucket-wise micro-batch is open. */
+smpu_status smpu_accumulate(smpu_ctx* ctx, const void* micro_grads, int64_t ntokens, void* stream);
+
+/* Bucket-wise micro-batch, for overlap with a still-running backward: micro_begin, then
+ * exactly one accumulate_bucket per bucket in any order (buckets are all-reduced in canonical bucket
+ * order on every rank).  bucket_grads: host or device fp16 of bucket b only
+ * (bucket_begin[b+1]-bucket_begin[b] elements).  ESTATE on a repeated bucket or a missing micro_begin. */
+smpu_status smpu_micro_begin(smpu_ctx* ctx, int64_t ntokens);
+smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* bucket_grads, void* stream);
+
+/* Finish the update: overflow decision, scaler, LR, fused unscale/normalise/Adam/re-cast, all on the
+ * device in stream order on `stream` (no host synchronisation).  ESTATE unless exactly c micro-batches
+ * (every bucket of the last one) were given.  out != NULL: wait for the update and fill *out
+ * (returns ESTATE if N was 0: the update was discarded).  out == NULL: asynchronous; fetch the result
+ * later with smpu_result. */
+smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out);
+
+/* Result of update attempt `attempt` (1-based; one of the last 64).  Waits for it. */
+smpu_status smpu_result(smpu_ctx* ctx, int64_t attempt, smpu_step_result* out);
+
+/* Copy theta (fp32[n]) to dst (host or device); synchronises the ctx's work first. */
+smpu_status smpu_get_master(smpu_ctx* ctx, float* dst, int64_t n);
+
+/* Read / write one state array (see SMPU_STATE_*); `bytes` must equal its size.  Synchronising.
+ * Writing MASTER does not touch W16 (write both to resume).  Refused (ESTATE) mid-update. */
+smpu_status smpu_get_state(smpu_ctx* ctx, int which, void* dst, int64_t bytes);
+smpu_status smpu_set_state(smpu_ctx* ctx, int which, const void* src, int64_t bytes);
+
+/* Per-kernel instrumentation (bench): enable=1 records CUDA events around every library launch on the
+ * stream it is launched on.  smpu_kernel_stats returns, per kernel id, the launch count since init and
+ * (when timing was on) the summed device time in ms; it synchronises. */
+smpu_status smpu_set_timing(smpu_ctx* ctx, int enable);
+smpu_status smpu_kernel_stats(smpu_ctx* ctx, int64_t* launches /* [SMPU_N_KERNELS] */,
+                              double* total_ms /* [SMPU_N_KERNELS] or NULL */, int reset);
+
+const char* smpu_last_error(void);
+void smpu_destroy(smpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMPU_H */

@@ -207,8 +207,8 @@ def full_overflow(wl, lay, u: int, e: int, chunk: int = 1 << 22) -> bool:
     import synth
     W, c = wl.world, wl.update_freq
     for lo in range(0, lay.n, chunk):
-        idx = np.arange(lo, min(lay.n, lo + chunk), dtype=np.int64)
-        accs = [accumulate([synth.micro_grad_sample(wl, lay, idx, u, r, k, e) for k in range(1, c + 1)])
+        hi = min(lay.n, lo + chunk)
+        accs = [accumulate([synth.micro_grad_range(wl, lay, lo, hi, u, r, k, e) for k in range(1, c + 1)])
                 for r in range(W)]
         if count_nonfinite(reduce(accs)) > 0:
             return True

@@ -1,0 +1,356 @@
+// kernels.cuh -- the sm_100a kernels of the update step (private to libsmpu.so).
+//
+//   K1   accumulate   A = g (first micro-batch) | A = rn16(A + g) (later ones), optional overflow test of
+//                     the OUTPUT A (finite + finite can overflow: 65504 + 16 -> inf).
+//   K1s  sweep        overflow test of the reduced bucket R after its all-reduce (W > 1).    P:158, reading R4
+//   K0   decide       one thread: flag -> skip/apply, dynamic loss scaler, t, lr(t), Adam scalars, result
+//                     record, next loss scale.
+//   K2   adam         fused unscale + normalise by N + Adam (fp32 master) + fp16 re-cast; every CTA exits
+//                     before any store when K0 decided to skip.
+//   Kc   cast         w16 = rn16(theta) (init / set_state only).
+//
+// All of them are HBM-streaming: 256-bit (v8.b32) global accesses (sm_100a LDG/STG.256), L1 no-allocate,
+// grid-stride over 32-byte vector units with two units in flight per thread.  Overflow test on packed
+// fp16 words: ((w & 0x7C007C00) + 0x04000400) & 0x80008000 is non-zero iff a half has exponent 0x1F.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "smpu.h"
+
+namespace smpu {
+
+struct __align__(32) V8 { uint32_t w[8]; };   // 32 B: 16 halves or 8 floats
+struct __align__(16) V4 { uint32_t w[4]; };   // 16 B: 8 halves
+
+// ---------------------------------------------------------------------------------------------- memory ops
+__device__ __forceinline__ V8 ld256_ro(const void* p) {          // read-only for the whole kernel
+    V8 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                   "=r"(r.w[6]), "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ V8 ld256(const void* p) {             // read then written by the same thread
+    V8 r;
+    asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                   "=r"(r.w[6]), "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st256(void* p, const V8& v) {
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+                 "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+__device__ __forceinline__ V4 ld128_ro(const void* p) {
+    V4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st128(void* p, const V4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                 "r"(v.w[2]), "r"(v.w[3])
+                 : "memory");
+}
+
+// fp16x2 add, round-to-nearest-even, never contracted (reading R1)
+__device__ __forceinline__ uint32_t hadd2_rn(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t nonfinite_bits(uint32_t w) {
+    return ((w & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
+}
+__device__ __forceinline__ bool h_nonfinite(uint16_t h) { return (h & 0x7C00u) == 0x7C00u; }
+
+__device__ __forceinline__ void raise_flag(bool bad, int* flag) {
+    // one store per warp that saw a non-finite value; every writer stores 1, so no atomics are needed
+    unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == (unsigned)(__ffs(any) - 1)) *(volatile int*)flag = 1;
+}
+
+// ---------------------------------------------------------------------------------------------- K1
+// acc[lo, hi) (absolute indices) <- g[0, hi-lo) (+ acc).  Vector path when acc+i and g+(i-lo) are
+// both 32-B aligned at the first 16-element boundary i >= lo, else an element path (correct, slower).
+template <bool FIRST, bool DETECT>
+__global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc, const uint16_t* __restrict__ g,
+                                                     int64_t lo, int64_t hi, int* __restrict__ flag) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const uint16_t* gb = g - lo;                       // gb[i] is the gradient of element i
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    bool vec_ok = ((reinterpret_cast<uintptr_t>(gb + vbeg) & 31) == 0);
+    int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
+    int64_t vend = vbeg + nvec * 16;
+    uint32_t bad = 0;
+    if (vec_ok) {
+        // body: 16 halves per unit, two units per thread in flight
+        int64_t u = tid;
+        for (; u + nthr < nvec; u += 2 * nthr) {
+            const int64_t i0 = vbeg + u * 16, i1 = vbeg + (u + nthr) * 16;
+            V8 g0 = ld256_ro(gb + i0), g1 = ld256_ro(gb + i1);
+            if (!FIRST) {
+                V8 a0 = ld256(acc + i0), a1 = ld256(acc + i1);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) { g0.w[j] = hadd2_rn(a0.w[j], g0.w[j]); g1.w[j] = hadd2_rn(a1.w[j], g1.w[j]); }
+            }
+            if (DETECT) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(g0.w[j]) | nonfinite_bits(g1.w[j]);
+            }
+            st256(acc + i0, g0);
+            st256(acc + i1, g1);
+        }
+        if (u < nvec) {
+            const int64_t i0 = vbeg + u * 16;
+            V8 g0 = ld256_ro(gb + i0);
+            if (!FIRST) {
+                V8 a0 = ld256(acc + i0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g0.w[j] = hadd2_rn(a0.w[j], g0.w[j]);
+            }
+            if (DETECT) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(g0.w[j]);
+            }
+            st256(acc + i0, g0);
+        }
+    }
+    // element path: head [lo, vbeg) and tail [vend, hi) -- or everything when not co-aligned
+    auto elem = [&](int64_t i) {
+        uint16_t x = gb[i];
+        if (!FIRST) {
+            uint32_t s = hadd2_rn((uint32_t)acc[i], (uint32_t)x);
+            x = (uint16_t)(s & 0xFFFFu);
+        }
+        if (DETECT && h_nonfinite(x)) bad |= 1u;
+        acc[i] = x;
+    };
+    if (vec_ok) {
+        for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+        for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
+    }
+    if (DETECT) raise_flag(bad != 0, flag);
+}
+
+// ---------------------------------------------------------------------------------------------- K1s
+__global__ void __launch_bounds__(256) k1s_sweep(const uint16_t* __restrict__ R, int64_t lo, int64_t hi,
+                                                 int* __restrict__ flag) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    int64_t nvec = (hi - vbeg) / 16, vend = vbeg + nvec * 16;
+    uint32_t bad = 0;
+    int64_t u = tid;
+    for (; u + nthr < nvec; u += 2 * nthr) {
+        V8 a = ld256_ro(R + vbeg + u * 16), b = ld256_ro(R + vbeg + (u + nthr) * 16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(a.w[j]) | nonfinite_bits(b.w[j]);
+    }
+    if (u < nvec) {
+        V8 a = ld256_ro(R + vbeg + u * 16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(a.w[j]);
+    }
+    for (int64_t i = lo + tid; i < vbeg; i += nthr) bad |= h_nonfinite(R[i]);
+    for (int64_t i = vend + tid; i < hi; i += nthr) bad |= h_nonfinite(R[i]);
+    raise_flag(bad != 0, flag);
+}
+
+// ---------------------------------------------------------------------------------------------- K0
+struct DevState {          // device-resident scaler / optimizer counters
+    int64_t e;             // scale exponent (scale = 2^e)
+    int64_t clean;         // consecutive clean updates
+    int64_t t;             // applied updates
+    int64_t attempts;      // update attempts
+};
+
+struct Scalars {           // written by K0, read by every K2 CTA
+    int32_t skip;
+    float inv_sN;          // fp32(1 / (2^e * N))
+    float step;            // fp32(lr / bc1)
+    float inv_sqrt_bc2;    // fp32(1 / sqrt(bc2))
+    float b1, omb1, b2, omb2, eps;
+};
+
+struct DevCfg {
+    double peak_lr;
+    int64_t warmup;
+    double beta1, beta2, eps;
+    int32_t emin, emax;
+    int64_t growth;
+};
+
+// lr(t) = peak * min(t / warmup, sqrt(warmup / t)) in fp64 (IEEE div/sqrt/mul, no contraction), one
+// rounding to fp32 (reading R14).
+__device__ __forceinline__ float lr_at(int64_t t, const DevCfg& c) {
+    double tt = (double)t, w = (double)c.warmup;
+    double lin = __ddiv_rn(tt, w);
+    double isq = __dsqrt_rn(__ddiv_rn(w, tt));
+    double f = lin < isq ? lin : isq;
+    return __double2float_rn(__dmul_rn(c.peak_lr, f));
+}
+
+__global__ void k0_decide(int* __restrict__ flag, const int64_t* __restrict__ dev_tokens, int64_t local_tokens,
+                          int use_dev_tokens, DevState* __restrict__ st, Scalars* __restrict__ sc,
+                          float* __restrict__ loss_scale, smpu_step_result* __restrict__ ring, int ring_mask,
+                          DevCfg cfg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int overflow = *(volatile int*)flag != 0;
+    *(volatile int*)flag = 0;                          // re-armed for the next update
+    const int64_t N = use_dev_tokens ? *dev_tokens : local_tokens;
+    DevState s = *st;
+    smpu_step_result r;
+    r.attempt = ++s.attempts;
+    r.overflow = overflow;
+    r.scale_log2_used = (int32_t)s.e;
+    r.ntokens_total = N;
+    r.discarded = 0;
+    int skip;
+    if (N <= 0) {                                      // reading R19: nothing changes
+        skip = 1;
+        r.discarded = 1;
+        r.applied = 0;
+        r.lr = lr_at(s.t + 1, cfg);
+    } else if (overflow) {                             // P:158 "scales down the loss when overflow is detected"
+        skip = 1;
+        s.e = s.e - 1 < cfg.emin ? cfg.emin : s.e - 1;
+        s.clean = 0;
+        r.applied = 0;
+        r.lr = lr_at(s.t + 1, cfg);                    // reading R15
+    } else {
+        skip = 0;
+        s.t += 1;
+        s.clean += 1;
+        r.applied = 1;
+        r.lr = lr_at(s.t, cfg);
+        // Adam scalars for this update, from the exponent the gradients carry (before growth)
+        double sN = ldexp((double)N, (int)r.scale_log2_used);
+        double bc1 = 1.0 - pow(cfg.beta1, (double)s.t);
+        double bc2 = 1.0 - pow(cfg.beta2, (double)s.t);
+        sc->inv_sN = __double2float_rn(1.0 / sN);
+        sc->step = __double2float_rn((double)r.lr / bc1);
+        sc->inv_sqrt_bc2 = __double2float_rn(1.0 / sqrt(bc2));
+        sc->b1 = (float)cfg.beta1;
+        sc->omb1 = (float)(1.0 - cfg.beta1);
+        sc->b2 = (float)cfg.beta2;
+        sc->omb2 = (float)(1.0 - cfg.beta2);
+        sc->eps = (float)cfg.eps;
+        if (s.clean >= cfg.growth) {                   // P:158 "scales the loss up if no overflows ... 2,000"
+            s.e = s.e + 1 > cfg.emax ? cfg.emax : s.e + 1;
+            s.clean = 0;
+        }
+    }
+    sc->skip = skip;
+    r.scale_log2_next = (int32_t)s.e;
+    r.num_updates = s.t;
+    r.clean_streak = s.clean;
+    *st = s;
+    *loss_scale = ldexpf(1.0f, (int)s.e);
+    ring[(r.attempt - 1) & ring_mask] = r;             // mapped pinned host memory
+    __threadfence_system();
+}
+
+// ---------------------------------------------------------------------------------------------- K2
+// Per element (Kingma & Ba Alg. 1 in torch's arrangement, reading R13):
+//   g = fp32(R) * inv_sN;  m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2
+//   theta -= step * m / (sqrt(v) * inv_sqrt_bc2 + eps);  w16 = rn16(theta)
+__device__ __forceinline__ void adam_elem(float R, float& th, float& m, float& v, const Scalars& s) {
+    float g = R * s.inv_sN;
+    m = s.b1 * m + s.omb1 * g;
+    v = s.b2 * v + s.omb2 * (g * g);
+    float denom = sqrtf(v) * s.inv_sqrt_bc2 + s.eps;
+    th = th - s.step * (m / denom);
+}
+
+__device__ __forceinline__ void adam_unit(const V4& r16, V8& th, V8& m, V8& v, V4& w16, const Scalars& s) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        __half2 rh = *reinterpret_cast<const __half2*>(&r16.w[j]);
+        float2 rf = __half22float2(rh);
+        float t0 = __uint_as_float(th.w[2 * j]), t1 = __uint_as_float(th.w[2 * j + 1]);
+        float m0 = __uint_as_float(m.w[2 * j]), m1 = __uint_as_float(m.w[2 * j + 1]);
+        float v0 = __uint_as_float(v.w[2 * j]), v1 = __uint_as_float(v.w[2 * j + 1]);
+        adam_elem(rf.x, t0, m0, v0, s);
+        adam_elem(rf.y, t1, m1, v1, s);
+        th.w[2 * j] = __float_as_uint(t0);
+        th.w[2 * j + 1] = __float_as_uint(t1);
+        m.w[2 * j] = __float_as_uint(m0);
+        m.w[2 * j + 1] = __float_as_uint(m1);
+        v.w[2 * j] = __float_as_uint(v0);
+        v.w[2 * j + 1] = __float_as_uint(v1);
+        __half2 wh = __floats2half2_rn(t0, t1);
+        w16.w[j] = *reinterpret_cast<uint32_t*>(&wh);
+    }
+}
+
+__global__ void __launch_bounds__(256) k2_adam(float* __restrict__ theta, float* __restrict__ m,
+                                               float* __restrict__ v, uint16_t* __restrict__ w16,
+                                               const uint16_t* __restrict__ R, int64_t n,
+                                               const Scalars* __restrict__ scp) {
+    if (*(volatile const int32_t*)&scp->skip) return;  // skipped update: no store at all (R6)
+    const Scalars s = *scp;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nvec = n / 8;                        // 8 elements per unit
+    int64_t u = tid;
+    for (; u + nthr < nvec; u += 2 * nthr) {
+        const int64_t i0 = u * 8, i1 = (u + nthr) * 8;
+        V4 r0 = ld128_ro(R + i0), r1 = ld128_ro(R + i1);
+        V8 t0 = ld256(theta + i0), t1 = ld256(theta + i1);
+        V8 m0 = ld256(m + i0), m1 = ld256(m + i1);
+        V8 v0 = ld256(v + i0), v1 = ld256(v + i1);
+        V4 w0, w1;
+        adam_unit(r0, t0, m0, v0, w0, s);
+        adam_unit(r1, t1, m1, v1, w1, s);
+        st256(theta + i0, t0);
+        st256(m + i0, m0);
+        st256(v + i0, v0);
+        st128(w16 + i0, w0);
+        st256(theta + i1, t1);
+        st256(m + i1, m1);
+        st256(v + i1, v1);
+        st128(w16 + i1, w1);
+    }
+    if (u < nvec) {
+        const int64_t i0 = u * 8;
+        V4 r0 = ld128_ro(R + i0);
+        V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
+        V4 w0;
+        adam_unit(r0, t0, m0, v0, w0, s);
+        st256(theta + i0, t0);
+        st256(m + i0, m0);
+        st256(v + i0, v0);
+        st128(w16 + i0, w0);
+    }
+    for (int64_t i = nvec * 8 + tid; i < n; i += nthr) {
+        float th = theta[i], mm = m[i], vv = v[i];
+        adam_elem(__half2float(__ushort_as_half(R[i])), th, mm, vv, s);
+        theta[i] = th;
+        m[i] = mm;
+        v[i] = vv;
+        w16[i] = __half_as_ushort(__float2half_rn(th));
+    }
+}
+
+// ---------------------------------------------------------------------------------------------- Kc
+__global__ void kc_cast(const float* __restrict__ theta, uint16_t* __restrict__ w16, int64_t n) {
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr)
+        w16[i] = __half_as_ushort(__float2half_rn(theta[i]));
+}
+
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+}  // namespace smpu

@@ -1,0 +1,732 @@
+// smpu.cu -- host engine and C ABI of libsmpu.so (see include/smpu.h for the contract).
+//
+// Layout in HBM (one allocation per array, 16 B per parameter in total):
+//   theta fp32[n], m fp32[n], v fp32[n]       fp32 master weights + Adam moments
+//   w16   fp16[n]                             fp16 model weights, re-cast each update
+//   acc   fp16[n]                             accumulator; buckets are views of it
+//   flag int32, tokens int64, DevState, Scalars, loss scale fp32   (device scalars; K0 owns them)
+//   result ring: 64 smpu_step_result in mapped pinned host memory (written by K0).
+//
+// Streams: K1 runs on the caller's stream; per-bucket NCCL all-reduce + K1s run on a high-priority
+// comm stream gated by one ready event per bucket (the paper's "background thread", becomes a
+// stream: enqueue is already asynchronous); K0 + K2 run on the stream given to smpu_step after it waits
+// for the comm stream.  No host synchronisation anywhere on the update path.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "smpu.h"
+
+using namespace smpu;
+
+namespace {
+
+thread_local std::string g_err;
+constexpr int kRing = 64;
+constexpr int64_t kStageElems = int64_t(16) << 20;   // 32 MiB of fp16 per host-staging buffer
+
+smpu_status set_err(smpu_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+enum PtrKind { PTR_DEVICE, PTR_HOST };
+
+}  // namespace
+
+struct smpu_ctx {
+    smpu_config cfg{};
+    int world = 1, rank = 0, dev = 0;
+    int64_t n = 0;
+    std::vector<int64_t> bbegin;   // bucket element offsets, size nb+1
+    int nb = 0;
+
+    float *theta = nullptr, *m = nullptr, *v = nullptr;
+    uint16_t *w16 = nullptr, *acc = nullptr;
+    int* flag = nullptr;
+    int64_t* tokens = nullptr;
+    DevState* st = nullptr;
+    Scalars* sc = nullptr;
+    float* scale = nullptr;
+    smpu_step_result* ring_host = nullptr;
+    smpu_step_result* ring_dev = nullptr;
+    cudaEvent_t ring_ev[kRing] = {};
+    DevCfg dcfg{};
+
+    ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr, copy_stream = nullptr;
+    std::vector<cudaEvent_t> ready;
+    cudaEvent_t comm_done = nullptr, order_ev = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool have_order = false;
+
+    uint16_t* stage[2] = {nullptr, nullptr};
+    cudaEvent_t stage_free[2] = {}, stage_full[2] = {};
+    int64_t stage_count = 0;
+
+    // update-in-progress bookkeeping (host)
+    int micro = 0;                 // micro-batches started in this update
+    bool bucket_micro = false;     // the open micro-batch is bucket-wise
+    std::vector<char> bucket_done;
+    int buckets_left = 0;
+    int next_issue = 0;
+    int64_t local_tokens = 0;
+    int64_t attempts = 0;
+    bool poisoned = false;
+
+    int grid_k1 = 0, grid_k2 = 0, grid_k1s = 0;
+
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[SMPU_N_KERNELS];
+    int64_t launches[SMPU_N_KERNELS] = {};
+};
+
+namespace {
+
+smpu_status fail_cuda(smpu_ctx* c, cudaError_t e, const char* what, int line) {
+    if (c) c->poisoned = true;
+    return set_err(SMPU_ECUDA, "CUDA error %d (%s) in %s at smpu.cu:%d", (int)e, cudaGetErrorString(e), what, line);
+}
+smpu_status fail_nccl(smpu_ctx* c, ncclResult_t e, const char* what, int line) {
+    if (c) c->poisoned = true;
+    return set_err(SMPU_ENCCL, "NCCL error %d (%s) in %s at smpu.cu:%d", (int)e, ncclGetErrorString(e), what, line);
+}
+
+#define CK(x)                                                        \
+    do {                                                             \
+        cudaError_t e_ = (x);                                        \
+        if (e_ != cudaSuccess) return fail_cuda(ctx, e_, #x, __LINE__); \
+    } while (0)
+#define CKL(what)                                                              \
+    do {                                                                       \
+        cudaError_t e_ = cudaGetLastError();                                   \
+        if (e_ != cudaSuccess) return fail_cuda(ctx, e_, what, __LINE__);      \
+    } while (0)
+#define NK(x)                                                        \
+    do {                                                             \
+        ncclResult_t r_ = (x);                                       \
+        if (r_ != ncclSuccess) return fail_nccl(ctx, r_, #x, __LINE__); \
+    } while (0)
+#define LIVE(ctx)                                                                             \
+    do {                                                                                      \
+        if (!(ctx)) return set_err(SMPU_EINVAL, "null ctx");                                  \
+        if ((ctx)->poisoned) return set_err(SMPU_EPOISONED, "ctx poisoned by an earlier error"); \
+    } while (0)
+
+PtrKind classify(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return PTR_HOST;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? PTR_DEVICE : PTR_HOST;
+}
+
+cudaEvent_t pool_event(smpu_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
+// bracket one launch with events when timing is on
+struct Timed {
+    smpu_ctx* c;
+    int kind;
+    cudaStream_t s;
+    cudaEvent_t b = nullptr;
+    Timed(smpu_ctx* c_, int k, cudaStream_t s_) : c(c_), kind(k), s(s_) {
+        c->launches[kind]++;
+        if (c->timing && (b = pool_event(c))) cudaEventRecord(b, s);
+    }
+    ~Timed() {
+        if (b) {
+            cudaEvent_t e = pool_event(c);
+            if (e) {
+                cudaEventRecord(e, s);
+                c->timed[kind].emplace_back(b, e);
+            }
+        }
+    }
+};
+
+// order this call's launches after the library's previous writes, whatever stream they were on
+smpu_status enter_stream(smpu_ctx* ctx, cudaStream_t s) {
+    if (ctx->have_order && s != ctx->last_stream) CK(cudaStreamWaitEvent(s, ctx->order_ev, 0));
+    return SMPU_OK;
+}
+smpu_status leave_stream(smpu_ctx* ctx, cudaStream_t s) {
+    CK(cudaEventRecord(ctx->order_ev, s));
+    ctx->last_stream = s;
+    ctx->have_order = true;
+    return SMPU_OK;
+}
+
+int grid_for(int64_t units, int max_grid) {
+    int64_t g = (units + 255) / 256;
+    if (g > max_grid) g = max_grid;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, bool first, bool detect,
+                      cudaStream_t s) {
+    if (hi <= lo) return SMPU_OK;
+    int grid = grid_for((hi - lo + 15) / 16, ctx->grid_k1);
+    Timed t(ctx, first ? SMPU_K1_FIRST : SMPU_K1_ADD, s);
+    if (first) {
+        if (detect) k1_accumulate<true, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
+        else k1_accumulate<true, false><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
+    } else {
+        if (detect) k1_accumulate<false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
+        else k1_accumulate<false, false><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
+    }
+    CKL("k1_accumulate");
+    return SMPU_OK;
+}
+
+// accumulate src (host or device) into acc[lo, hi)
+smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, bool first, bool detect,
+                             cudaStream_t s) {
+    if (classify(src) == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s);
+    // host memory: double-buffered H2D staging on the copy stream, overlapped with K1 on `s`
+    for (int64_t c0 = lo; c0 < hi; c0 += kStageElems) {
+        int64_t c1 = c0 + kStageElems < hi ? c0 + kStageElems : hi;
+        int j = (int)(ctx->stage_count++ & 1);
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->stage_free[j], 0));
+        CK(cudaMemcpyAsync(ctx->stage[j], src + (c0 - lo), (size_t)(c1 - c0) * 2, cudaMemcpyHostToDevice,
+                           ctx->copy_stream));
+        CK(cudaEventRecord(ctx->stage_full[j], ctx->copy_stream));
+        CK(cudaStreamWaitEvent(s, ctx->stage_full[j], 0));
+        // the staging buffer holds elements [c0, c1): index it relative to c0
+        smpu_status st = launch_k1(ctx, ctx->stage[j], c0, c1, first, detect, s);
+        if (st != SMPU_OK) return st;
+        CK(cudaEventRecord(ctx->stage_free[j], s));
+    }
+    return SMPU_OK;
+}
+
+// issue, in canonical bucket order, the all-reduces of every bucket whose final-micro K1 is enqueued
+smpu_status issue_ready_buckets(smpu_ctx* ctx) {
+    while (ctx->next_issue < ctx->nb && ctx->bucket_done[ctx->next_issue]) {
+        int b = ctx->next_issue;
+        int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
+        cudaStream_t cs = ctx->comm_stream;
+        CK(cudaStreamWaitEvent(cs, ctx->ready[b], 0));
+        if (b == 0) {   // global token count N = sum_r N_r, issued with the first bucket
+            k_set_i64<<<1, 1, 0, cs>>>(ctx->tokens, ctx->local_tokens);
+            CKL("k_set_i64");
+            NK(ncclAllReduce(ctx->tokens, ctx->tokens, 1, ncclInt64, ncclSum, ctx->comm, cs));
+        }
+        {
+            Timed t(ctx, SMPU_NCCL_AR, cs);
+            NK(ncclAllReduce(ctx->acc + lo, ctx->acc + lo, (size_t)(hi - lo), ncclFloat16, ncclSum, ctx->comm, cs));
+        }
+        {
+            Timed t(ctx, SMPU_K1S, cs);
+            k1s_sweep<<<grid_for((hi - lo + 15) / 16, ctx->grid_k1s), 256, 0, cs>>>(ctx->acc, lo, hi, ctx->flag);
+            CKL("k1s_sweep");
+        }
+        ctx->next_issue++;
+    }
+    if (ctx->next_issue == ctx->nb) CK(cudaEventRecord(ctx->comm_done, ctx->comm_stream));
+    return SMPU_OK;
+}
+
+smpu_status plan(const int64_t* numel, int n_tensors, int64_t bucket_bytes, std::vector<int64_t>& out) {
+    out.clear();
+    out.push_back(0);
+    int64_t off = 0, cur = 0;
+    for (int j = 0; j < n_tensors; ++j) {
+        if (numel[j] <= 0) return set_err(SMPU_EINVAL, "numel[%d] = %lld must be > 0", j, (long long)numel[j]);
+        off += numel[j];
+        cur += numel[j] * 2;
+        if (cur >= bucket_bytes) {   // close at >= threshold (reading R17)
+            out.push_back(off);
+            cur = 0;
+        }
+    }
+    if (out.back() != off) out.push_back(off);
+    return SMPU_OK;
+}
+
+smpu_status check_cfg(const smpu_config* c) {
+    if (!c) return set_err(SMPU_EINVAL, "null cfg");
+    if (c->update_freq < 1) return set_err(SMPU_EINVAL, "update_freq must be >= 1");
+    if (c->warmup_updates < 1) return set_err(SMPU_EINVAL, "warmup_updates must be >= 1");
+    if (!(c->peak_lr > 0) || !(c->beta1 >= 0 && c->beta1 < 1) || !(c->beta2 >= 0 && c->beta2 < 1) || !(c->eps > 0))
+        return set_err(SMPU_EINVAL, "bad Adam / lr hyper-parameters");
+    if (c->min_scale_log2 > c->init_scale_log2 || c->init_scale_log2 > c->max_scale_log2 ||
+        c->min_scale_log2 < -120 || c->max_scale_log2 > 120)
+        return set_err(SMPU_EINVAL, "need min_scale_log2 <= init_scale_log2 <= max_scale_log2 within +-120");
+    if (c->growth_interval < 1) return set_err(SMPU_EINVAL, "growth_interval must be >= 1");
+    if (c->bucket_bytes < 2) return set_err(SMPU_EINVAL, "bucket_bytes must be >= 2");
+    return SMPU_OK;
+}
+
+void free_ctx(smpu_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    cudaDeviceSynchronize();
+    if (c->comm) ncclCommDestroy(c->comm);
+    cudaFree(c->theta);
+    cudaFree(c->m);
+    cudaFree(c->v);
+    cudaFree(c->w16);
+    cudaFree(c->acc);
+    cudaFree(c->flag);
+    cudaFree(c->tokens);
+    cudaFree(c->st);
+    cudaFree(c->sc);
+    cudaFree(c->scale);
+    cudaFree(c->stage[0]);
+    cudaFree(c->stage[1]);
+    if (c->ring_host) cudaFreeHost(c->ring_host);
+    for (auto& e : c->ring_ev) if (e) cudaEventDestroy(e);
+    for (auto& e : c->ready) if (e) cudaEventDestroy(e);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (int j = 0; j < 2; ++j) {
+        if (c->stage_free[j]) cudaEventDestroy(c->stage_free[j]);
+        if (c->stage_full[j]) cudaEventDestroy(c->stage_full[j]);
+    }
+    if (c->comm_done) cudaEventDestroy(c->comm_done);
+    if (c->order_ev) cudaEventDestroy(c->order_ev);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    delete c;
+}
+
+void start_micro(smpu_ctx* c, int64_t ntokens) {
+    c->micro++;
+    c->local_tokens += ntokens;
+}
+
+bool final_micro(const smpu_ctx* c) { return c->micro == c->cfg.update_freq; }
+
+}  // namespace
+
+// ================================================================================================ C ABI
+extern "C" {
+
+int smpu_abi_version(void) { return SMPU_ABI_VERSION; }
+
+const char* smpu_last_error(void) { return g_err.c_str(); }
+
+smpu_status smpu_config_default(smpu_config* c) {
+    if (!c) return set_err(SMPU_EINVAL, "null cfg");
+    c->peak_lr = 5e-4;
+    c->warmup_updates = 4000;
+    c->beta1 = 0.9;
+    c->beta2 = 0.98;
+    c->eps = 1e-8;
+    c->init_scale_log2 = 7;
+    c->min_scale_log2 = -5;
+    c->max_scale_log2 = 24;
+    c->growth_interval = 2000;
+    c->update_freq = 1;
+    c->bucket_bytes = int64_t(150) << 20;
+    return SMPU_OK;
+}
+
+smpu_status smpu_unique_id(void* out, int64_t bytes) {
+    smpu_ctx* ctx = nullptr;
+    if (!out || bytes < (int64_t)sizeof(ncclUniqueId)) return set_err(SMPU_EINVAL, "need a >= 128-byte buffer");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    memcpy(out, &id, sizeof id);
+    return SMPU_OK;
+}
+
+smpu_status smpu_plan_buckets(const int64_t* numel, int n_tensors, int64_t bucket_bytes, int* n_buckets,
+                              int64_t* bucket_begin) {
+    if (!numel || n_tensors < 1 || !n_buckets || bucket_bytes < 2) return set_err(SMPU_EINVAL, "bad arguments");
+    std::vector<int64_t> b;
+    smpu_status s = plan(numel, n_tensors, bucket_bytes, b);
+    if (s != SMPU_OK) return s;
+    *n_buckets = (int)b.size() - 1;
+    if (bucket_begin) memcpy(bucket_begin, b.data(), b.size() * sizeof(int64_t));
+    return SMPU_OK;
+}
+
+smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
+                      int cuda_device, const int64_t* numel, int n_tensors, const float* init_params) {
+    if (!out) return set_err(SMPU_EINVAL, "null out");
+    *out = nullptr;
+    smpu_status s = check_cfg(cfg);
+    if (s != SMPU_OK) return s;
+    if (world < 1 || rank < 0 || rank >= world) return set_err(SMPU_EINVAL, "need 0 <= rank < world");
+    if (world > 1 && !nccl_id) return set_err(SMPU_EINVAL, "world > 1 needs an NCCL unique id");
+    if (!numel || n_tensors < 1 || !init_params) return set_err(SMPU_EINVAL, "null tensor list / params");
+
+    smpu_ctx* ctx = new smpu_ctx();
+    ctx->cfg = *cfg;
+    ctx->world = world;
+    ctx->rank = rank;
+    ctx->dev = cuda_device;
+    s = plan(numel, n_tensors, cfg->bucket_bytes, ctx->bbegin);
+    if (s != SMPU_OK) {
+        delete ctx;
+        return s;
+    }
+    ctx->nb = (int)ctx->bbegin.size() - 1;
+    ctx->n = ctx->bbegin.back();
+    const int64_t n = ctx->n;
+
+    auto bail = [&](smpu_status st) {
+        std::string keep = g_err;
+        free_ctx(ctx);
+        g_err = keep;
+        return st;
+    };
+#define IK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            return bail(e_ == cudaErrorMemoryAllocation                                \
+                            ? set_err(SMPU_ENOMEM, "%s: out of memory", #x)            \
+                            : fail_cuda(nullptr, e_, #x, __LINE__));                   \
+    } while (0)
+
+    IK(cudaSetDevice(cuda_device));
+    cudaDeviceProp prop;
+    IK(cudaGetDeviceProperties(&prop, cuda_device));
+    if (prop.major != 10 || prop.minor != 0)
+        return bail(set_err(SMPU_EINVAL, "libsmpu.so is built for sm_100a (B200); device %d is sm_%d%d", cuda_device,
+                            prop.major, prop.minor));
+    IK(cudaMalloc(&ctx->theta, n * 4));
+    IK(cudaMalloc(&ctx->m, n * 4));
+    IK(cudaMalloc(&ctx->v, n * 4));
+    IK(cudaMalloc(&ctx->w16, n * 2));
+    IK(cudaMalloc(&ctx->acc, n * 2));
+    IK(cudaMalloc(&ctx->flag, sizeof(int)));
+    IK(cudaMalloc(&ctx->tokens, sizeof(int64_t)));
+    IK(cudaMalloc(&ctx->st, sizeof(DevState)));
+    IK(cudaMalloc(&ctx->sc, sizeof(Scalars)));
+    IK(cudaMalloc(&ctx->scale, sizeof(float)));
+    IK(cudaMalloc(&ctx->stage[0], kStageElems * 2));
+    IK(cudaMalloc(&ctx->stage[1], kStageElems * 2));
+    IK(cudaHostAlloc(&ctx->ring_host, kRing * sizeof(smpu_step_result), cudaHostAllocMapped));
+    IK(cudaHostGetDevicePointer((void**)&ctx->ring_dev, ctx->ring_host, 0));
+    memset(ctx->ring_host, 0, kRing * sizeof(smpu_step_result));
+    for (auto& e : ctx->ring_ev) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ready.resize(ctx->nb);
+    for (auto& e : ctx->ready) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->bucket_done.assign(ctx->nb, 0);
+    IK(cudaEventCreateWithFlags(&ctx->comm_done, cudaEventDisableTiming));
+    IK(cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming));
+    int lo_prio = 0, hi_prio = 0;
+    IK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    IK(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
+    IK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int j = 0; j < 2; ++j) {
+        IK(cudaEventCreateWithFlags(&ctx->stage_free[j], cudaEventDisableTiming));
+        IK(cudaEventCreateWithFlags(&ctx->stage_full[j], cudaEventDisableTiming));
+        IK(cudaEventRecord(ctx->stage_free[j], ctx->copy_stream));
+    }
+
+    // persistent grids: resident CTAs per SM x SMs
+    int occ = 0;
+    IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_accumulate<false, false>, 256, 0));
+    ctx->grid_k1 = prop.multiProcessorCount * (occ > 0 ? occ : 1);
+    IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_adam, 256, 0));
+    ctx->grid_k2 = prop.multiProcessorCount * (occ > 0 ? occ : 1);
+    IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1s_sweep, 256, 0));
+    ctx->grid_k1s = prop.multiProcessorCount * (occ > 0 ? occ : 1);
+
+    DevCfg& d = ctx->dcfg;
+    d.peak_lr = cfg->peak_lr;
+    d.warmup = cfg->warmup_updates;
+    d.beta1 = cfg->beta1;
+    d.beta2 = cfg->beta2;
+    d.eps = cfg->eps;
+    d.emin = cfg->min_scale_log2;
+    d.emax = cfg->max_scale_log2;
+    d.growth = cfg->growth_interval;
+
+    cudaStream_t s0 = ctx->copy_stream;
+    IK(cudaMemcpyAsync(ctx->theta, init_params, n * 4, cudaMemcpyDefault, s0));
+    IK(cudaMemsetAsync(ctx->m, 0, n * 4, s0));
+    IK(cudaMemsetAsync(ctx->v, 0, n * 4, s0));
+    IK(cudaMemsetAsync(ctx->acc, 0, n * 2, s0));
+    IK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), s0));
+    IK(cudaMemsetAsync(ctx->tokens, 0, sizeof(int64_t), s0));
+    IK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), s0));
+    DevState st0{cfg->init_scale_log2, 0, 0, 0};
+    IK(cudaMemcpyAsync(ctx->st, &st0, sizeof st0, cudaMemcpyHostToDevice, s0));
+    float sc0 = ldexpf(1.0f, cfg->init_scale_log2);
+    IK(cudaMemcpyAsync(ctx->scale, &sc0, sizeof sc0, cudaMemcpyHostToDevice, s0));
+    IK(cudaStreamSynchronize(s0));
+
+    if (world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
+        if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclCommInitRank", __LINE__));
+        // replicas start bitwise identical: rank 0's theta_0
+        r = ncclBroadcast(ctx->theta, ctx->theta, (size_t)n, ncclFloat32, 0, ctx->comm, s0);
+        if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclBroadcast", __LINE__));
+    }
+    kc_cast<<<grid_for(n, ctx->grid_k2), 256, 0, s0>>>(ctx->theta, ctx->w16, n);
+    ctx->launches[SMPU_KCAST]++;
+    IK(cudaGetLastError());
+    IK(cudaStreamSynchronize(s0));
+#undef IK
+    *out = ctx;
+    return SMPU_OK;
+}
+
+smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n) {
+    if (!ctx || !n) return set_err(SMPU_EINVAL, "null argument");
+    *n = ctx->n;
+    return SMPU_OK;
+}
+
+smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_begin) {
+    if (!ctx || !n_buckets) return set_err(SMPU_EINVAL, "null argument");
+    *n_buckets = ctx->nb;
+    if (bucket_begin) memcpy(bucket_begin, ctx->bbegin.data(), ctx->bbegin.size() * sizeof(int64_t));
+    return SMPU_OK;
+}
+
+smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16) {
+    if (!ctx || !dev_w16) return set_err(SMPU_EINVAL, "null argument");
+    *dev_w16 = ctx->w16;
+    return SMPU_OK;
+}
+
+smpu_status smpu_loss_scale(const smpu_ctx* ctx, const float** dev_scale) {
+    if (!ctx || !dev_scale) return set_err(SMPU_EINVAL, "null argument");
+    *dev_scale = ctx->scale;
+    return SMPU_OK;
+}
+
+smpu_status smpu_micro_begin(smpu_ctx* ctx, int64_t ntokens) {
+    LIVE(ctx);
+    if (ntokens < 0) return set_err(SMPU_EINVAL, "ntokens < 0");
+    if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "previous bucket-wise micro-batch still has %d buckets", ctx->buckets_left);
+    if (ctx->micro >= ctx->cfg.update_freq)
+        return set_err(SMPU_ESTATE, "already %d micro-batches this update; call smpu_step", ctx->micro);
+    CK(cudaSetDevice(ctx->dev));
+    start_micro(ctx, ntokens);
+    ctx->bucket_micro = true;
+    ctx->buckets_left = ctx->nb;
+    std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    return SMPU_OK;
+}
+
+smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads, void* stream) {
+    LIVE(ctx);
+    if (!ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_accumulate_bucket without smpu_micro_begin");
+    if (bucket < 0 || bucket >= ctx->nb) return set_err(SMPU_EINVAL, "bucket %d out of [0, %d)", bucket, ctx->nb);
+    if (!grads) return set_err(SMPU_EINVAL, "null grads");
+    if (ctx->bucket_done[bucket]) return set_err(SMPU_ESTATE, "bucket %d already given in this micro-batch", bucket);
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    smpu_status st = enter_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    const bool last = final_micro(ctx);
+    const bool first = ctx->micro == 1;
+    st = accumulate_range(ctx, (const uint16_t*)grads, ctx->bbegin[bucket], ctx->bbegin[bucket + 1], first,
+                          last && ctx->world == 1, s);
+    if (st != SMPU_OK) return st;
+    ctx->bucket_done[bucket] = 1;
+    if (last && ctx->world > 1) {
+        CK(cudaEventRecord(ctx->ready[bucket], s));
+        st = issue_ready_buckets(ctx);
+        if (st != SMPU_OK) return st;
+    }
+    st = leave_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    if (--ctx->buckets_left == 0) ctx->bucket_micro = false;
+    return SMPU_OK;
+}
+
+smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, void* stream) {
+    LIVE(ctx);
+    if (!grads) return set_err(SMPU_EINVAL, "null grads");
+    if (ntokens < 0) return set_err(SMPU_EINVAL, "ntokens < 0");
+    if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "a bucket-wise micro-batch is open");
+    if (ctx->micro >= ctx->cfg.update_freq)
+        return set_err(SMPU_ESTATE, "already %d micro-batches this update; call smpu_step", ctx->micro);
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ctx->micro + 1 == ctx->cfg.update_freq && ctx->world > 1) {
+        // final micro-batch of a multi-GPU update: bucket by bucket, so that bucket b's all-reduce
+        // overlaps the accumulation of buckets > b
+        smpu_status st = smpu_micro_begin(ctx, ntokens);
+        if (st != SMPU_OK) return st;
+        const uint16_t* g = (const uint16_t*)grads;
+        for (int b = 0; b < ctx->nb; ++b) {
+            st = smpu_accumulate_bucket(ctx, b, g + ctx->bbegin[b], stream);
+            if (st != SMPU_OK) return st;
+        }
+        return SMPU_OK;
+    }
+    smpu_status st = enter_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    start_micro(ctx, ntokens);
+    const bool last = final_micro(ctx);
+    st = accumulate_range(ctx, (const uint16_t*)grads, 0, ctx->n, ctx->micro == 1, last, s);
+    if (st != SMPU_OK) return st;
+    return leave_stream(ctx, s);
+}
+
+smpu_status smpu_result(smpu_ctx* ctx, int64_t attempt, smpu_step_result* out) {
+    LIVE(ctx);
+    if (!out) return set_err(SMPU_EINVAL, "null out");
+    if (attempt < 1 || attempt > ctx->attempts || attempt <= ctx->attempts - kRing)
+        return set_err(SMPU_EINVAL, "attempt %lld not among the last %d (issued %lld)", (long long)attempt, kRing,
+                       (long long)ctx->attempts);
+    int slot = (int)((attempt - 1) % kRing);
+    CK(cudaEventSynchronize(ctx->ring_ev[slot]));
+    memcpy(out, (const void*)&ctx->ring_host[slot], sizeof *out);
+    return SMPU_OK;
+}
+
+smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
+    LIVE(ctx);
+    if (ctx->micro != ctx->cfg.update_freq || ctx->bucket_micro)
+        return set_err(SMPU_ESTATE, "smpu_step after %d of %d micro-batches%s", ctx->micro, ctx->cfg.update_freq,
+                       ctx->bucket_micro ? " (a bucket-wise micro-batch is incomplete)" : "");
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    smpu_status st = enter_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    if (ctx->world > 1) CK(cudaStreamWaitEvent(s, ctx->comm_done, 0));
+    {
+        Timed t(ctx, SMPU_K0, s);
+        k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->tokens, ctx->local_tokens, ctx->world > 1, ctx->st, ctx->sc,
+                                   ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg);
+        CKL("k0_decide");
+    }
+    {
+        Timed t(ctx, SMPU_K2, s);
+        k2_adam<<<grid_for((ctx->n + 7) / 8, ctx->grid_k2), 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
+                                                                         ctx->acc, ctx->n, ctx->sc);
+        CKL("k2_adam");
+    }
+    ctx->attempts++;
+    CK(cudaEventRecord(ctx->ring_ev[(ctx->attempts - 1) % kRing], s));
+    st = leave_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    ctx->micro = 0;
+    ctx->local_tokens = 0;
+    ctx->next_issue = 0;
+    std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    if (!out) return SMPU_OK;
+    st = smpu_result(ctx, ctx->attempts, out);
+    if (st != SMPU_OK) return st;
+    if (out->discarded) return set_err(SMPU_ESTATE, "N = 0 tokens in this update: discarded (reading R19)");
+    return SMPU_OK;
+}
+
+static smpu_status state_array(smpu_ctx* ctx, int which, void** p, int64_t* bytes) {
+    switch (which) {
+        case SMPU_STATE_MASTER: *p = ctx->theta; *bytes = ctx->n * 4; break;
+        case SMPU_STATE_M: *p = ctx->m; *bytes = ctx->n * 4; break;
+        case SMPU_STATE_V: *p = ctx->v; *bytes = ctx->n * 4; break;
+        case SMPU_STATE_W16: *p = ctx->w16; *bytes = ctx->n * 2; break;
+        case SMPU_STATE_ACCUM: *p = ctx->acc; *bytes = ctx->n * 2; break;
+        case SMPU_STATE_SCALARS: *p = ctx->st; *bytes = 4 * sizeof(int64_t); break;
+        default: return set_err(SMPU_EINVAL, "unknown state selector %d", which);
+    }
+    return SMPU_OK;
+}
+
+smpu_status smpu_get_state(smpu_ctx* ctx, int which, void* dst, int64_t bytes) {
+    LIVE(ctx);
+    if (!dst) return set_err(SMPU_EINVAL, "null dst");
+    void* p;
+    int64_t nb;
+    smpu_status s = state_array(ctx, which, &p, &nb);
+    if (s != SMPU_OK) return s;
+    if (bytes != nb) return set_err(SMPU_EINVAL, "state %d is %lld bytes, got %lld", which, (long long)nb, (long long)bytes);
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(dst, p, (size_t)nb, cudaMemcpyDefault));
+    return SMPU_OK;
+}
+
+smpu_status smpu_set_state(smpu_ctx* ctx, int which, const void* src, int64_t bytes) {
+    LIVE(ctx);
+    if (!src) return set_err(SMPU_EINVAL, "null src");
+    if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_set_state in the middle of an update");
+    void* p;
+    int64_t nb;
+    smpu_status s = state_array(ctx, which, &p, &nb);
+    if (s != SMPU_OK) return s;
+    if (bytes != nb) return set_err(SMPU_EINVAL, "state %d is %lld bytes, got %lld", which, (long long)nb, (long long)bytes);
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
+    if (which == SMPU_STATE_SCALARS) {
+        int64_t v[4];
+        memcpy(v, src, sizeof v);
+        if (v[0] < ctx->cfg.min_scale_log2 || v[0] > ctx->cfg.max_scale_log2 || v[1] < 0 || v[2] < 0 || v[3] < 0)
+            return set_err(SMPU_EINVAL, "scalar state out of range");
+        CK(cudaMemcpy(p, src, (size_t)nb, cudaMemcpyHostToDevice));
+        float sc = ldexpf(1.0f, (int)v[0]);
+        CK(cudaMemcpy(ctx->scale, &sc, sizeof sc, cudaMemcpyHostToDevice));
+        ctx->attempts = v[3];
+        return SMPU_OK;
+    }
+    CK(cudaMemcpy(p, src, (size_t)nb, cudaMemcpyDefault));
+    return SMPU_OK;
+}
+
+smpu_status smpu_get_master(smpu_ctx* ctx, float* dst, int64_t n) {
+    LIVE(ctx);
+    if (n != ctx->n) return set_err(SMPU_EINVAL, "n = %lld, ctx has %lld", (long long)n, (long long)ctx->n);
+    return smpu_get_state(ctx, SMPU_STATE_MASTER, dst, n * 4);
+}
+
+smpu_status smpu_set_timing(smpu_ctx* ctx, int enable) {
+    LIVE(ctx);
+    ctx->timing = enable != 0;
+    return SMPU_OK;
+}
+
+smpu_status smpu_kernel_stats(smpu_ctx* ctx, int64_t* launches, double* total_ms, int reset) {
+    LIVE(ctx);
+    if (!launches) return set_err(SMPU_EINVAL, "null launches");
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
+    for (int k = 0; k < SMPU_N_KERNELS; ++k) {
+        launches[k] = ctx->launches[k];
+        if (total_ms) {
+            double tot = 0;
+            for (auto& pr : ctx->timed[k]) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+                tot += ms;
+            }
+            total_ms[k] = tot;
+        }
+    }
+    if (reset) {
+        for (int k = 0; k < SMPU_N_KERNELS; ++k) {
+            ctx->launches[k] = 0;
+            ctx->timed[k].clear();
+        }
+        ctx->ev_used = 0;
+    }
+    return SMPU_OK;
+}
+
+void smpu_destroy(smpu_ctx* ctx) { free_ctx(ctx); }
+
+}  // extern "C"

@@ -37,6 +37,7 @@ def _load():
         lib.synth_ntokens.restype = i64
         lib.synth_ntokens.argtypes = [u64]
         lib.synth_fill.argtypes = [p, i32, p, p, i32, u64, i32, i32]
+        lib.synth_fill_range.argtypes = [p, i64, i64, i32, p, p, i32, u64, i32, i32]
         lib.synth_sample.argtypes = [p, p, i64, i32, p, p, i32, u64, i32, i32]
         lib.synth_theta0.argtypes = [p, i64, u64]
         lib.synth_theta0_sample.argtypes = [p, p, i64, u64]
@@ -132,6 +133,19 @@ def micro_grad_cpu(wl: Workload, lay: Layout, u: int, r: int, k: int, e: int, fa
                        key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq))
     for i, bits in overrides(wl, u, r, k):
         out[i] = bits
+    return out
+
+
+def micro_grad_range(wl: Workload, lay: Layout, lo: int, hi: int, u: int, r: int, k: int, e: int,
+                     family: str | None = None):
+    """g_{r,k}[lo:hi] (uint16 bit patterns), injections included."""
+    fam = FAMILIES[family or wl.family]
+    out = np.empty(hi - lo, dtype=np.uint16)
+    _load().synth_fill_range(_ptr(out), lo, hi, lay.n_tensors, _ptr(lay.begin), _ptr(lay.cls), fam,
+                             key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq))
+    for i, bits in overrides(wl, u, r, k):
+        if lo <= i < hi:
+            out[i - lo] = bits
     return out
 
 

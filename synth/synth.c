@@ -98,6 +98,18 @@ static int find_tensor(int n_tensors, const int64_t* tensor_begin, int64_t i) {
     return lo;
 }
 
+/* Elements [lo, hi) of the packed vector into out[0 .. hi-lo). */
+void synth_fill_range(uint16_t* out, int64_t lo, int64_t hi, int n_tensors, const int64_t* tensor_begin,
+                      const int32_t* cls, int family, uint64_t key, int e, int K) {
+    for (int j = 0; j < n_tensors; ++j) {
+        int64_t b = tensor_begin[j] > lo ? tensor_begin[j] : lo;
+        int64_t end = tensor_begin[j + 1] < hi ? tensor_begin[j + 1] : hi;
+        int c = cls[j];
+#pragma omp parallel for schedule(static)
+        for (int64_t i = b; i < end; ++i) out[i - lo] = gen_elem(key, i, family, c, e, K);
+    }
+}
+
 /* Values at arbitrary packed indices idx[0..m). */
 void synth_sample(uint16_t* out, const int64_t* idx, int64_t m, int n_tensors,
                   const int64_t* tensor_begin, const int32_t* cls, int family, uint64_t key, int e, int K) {

@@ -1,0 +1,89 @@
+"""The C ABI library loads and exports every symbol include/smpu.h declares; host-only calls (no GPU)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from synth import models
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def P():
+    so = os.path.join(ROOT, "paper_1806_00187_b200", "libsmpu.so")
+    if not os.path.exists(so):
+        import subprocess
+        import sys
+        subprocess.run([sys.executable, "-m", "paper_1806_00187_b200._build"], cwd=ROOT, check=True)
+    import paper_1806_00187_b200 as pkg
+    return pkg
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "smpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(smpu_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(P):
+    names = header_functions()
+    assert len(names) >= 20
+    lib = ctypes.CDLL(P.smpu.LIB_PATH)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(P.smpu.EXPORTS)   # the binding covers the whole header
+
+
+def test_abi_version_and_defaults(P):
+    assert P.abi_version() == 1
+    c = P.config_default()
+    assert (c.peak_lr, c.warmup_updates, c.beta1, c.beta2, c.eps) == (5e-4, 4000, 0.9, 0.98, 1e-8)
+    assert (c.init_scale_log2, c.min_scale_log2, c.max_scale_log2, c.growth_interval) == (7, -5, 24, 2000)
+    assert c.bucket_bytes == 150 << 20                                                                # P:212 fn
+
+
+# whole-tensor greedy buckets of Transformer-big En-De (count, last bucket MiB)
+A2 = {1: (61, 64.0), 2: (61, 64.0), 4: (43, 64.0), 8: (43, 64.0), 16: (22, 64.0), 32: (11, 80.0), 64: (6, 80.0),
+      128: (3, 144.1), 150: (3, 96.0), 256: (2, 144.1)}
+
+
+@pytest.mark.parametrize("mib", sorted(A2))
+def test_bucket_plan_big_ende(P, mib):
+    wl = models.big_ende()
+    b = P.plan_buckets(wl.numel, mib << 20)
+    nb, last = A2[mib]
+    assert len(b) - 1 == nb
+    assert round((b[-1] - b[-2]) * 2 / 2**20, 1) == last
+    assert b[0] == 0 and b[-1] == wl.n
+    # every bucket but the last reaches the threshold; boundaries are tensor boundaries (whole tensors)
+    sizes = np.diff(b) * 2
+    assert np.all(sizes[:-1] >= mib << 20)
+    ends = set(np.cumsum(wl.numel).tolist())
+    assert all(int(x) in ends for x in b[1:])
+
+
+def test_bucket_plan_150mib_paper_configs(P):
+    # "150MB" buckets: big En-De 152.2/152.2/96.0 MiB, big En-Fr 152.2/152.2/119.0, base 1 x 116.2
+    mib = lambda b: [round(x * 2 / 2**20, 1) for x in np.diff(b)]  # noqa: E731
+    assert mib(P.plan_buckets(models.big_ende().numel, 150 << 20)) == [152.2, 152.2, 96.0]
+    assert mib(P.plan_buckets(models.big_enfr().numel, 150 << 20)) == [152.2, 152.2, 119.0]
+    assert mib(P.plan_buckets(models.base_ende().numel, 150 << 20)) == [116.2]
+
+
+def test_bucket_plan_rejects_bad_input(P):
+    with pytest.raises(P.SmpuError) as ei:
+        P.plan_buckets([10, 0, 5], 100)
+    assert ei.value.status == P.smpu.EINVAL
+
+
+def test_product_has_no_oracle_dependency():
+    # the product path never imports / links the oracle (task rule)
+    pkg = os.path.join(ROOT, "paper_1806_00187_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower().replace("oracle-exact", ""), f

@@ -1,0 +1,245 @@
+"""CUDA path (libsmpu.so through its C ABI) vs the CPU oracle, element by element on the same seeded inputs.
+
+Bar (north_star): decisions (overflow, applied, e_used, e_next, lr bits, t, N, clean) bitwise
+every update; accumulator bitwise at W = 1; w16 within 1 fp16 ulp; theta/m/v within 1e-6 (operand-scale
+relative) after 1 update and 1e-4 after 100.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from synth import models
+from tests.gpu_util import (RTOL_1, RTOL_100, Magnitudes, check_state, decisions, gpu_state, h2t, lib_cfg,
+                            oracle_decisions, snapshot)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_1806_00187_b200 as pkg
+    return pkg
+
+
+def run_pair(P, wl, updates, *, ocfg=None, cfg_kw=None, mode="whole", rtol_last=None, check_every=True,
+             host_inputs=None, bucket_order=None):
+    """Run the library and the oracle (full vectors) side by side; compare after every update."""
+    import torch
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    ocfg = ocfg or O.Config()
+    orc = O.Oracle(theta0, ocfg)
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, ocfg, **(cfg_kw or {})))
+    assert step.n == lay.n
+    mags = Magnitudes(theta0)
+    applied = 0
+    for u in range(1, updates + 1):
+        e = orc.e
+        grads = [[synth.micro_grad_cpu(wl, lay, u, r, k, e) for k in range(1, wl.update_freq + 1)]
+                 for r in range(wl.world)]
+        toks = [[synth.ntokens(wl, u, r, k) for k in range(1, wl.update_freq + 1)] for r in range(wl.world)]
+        before = snapshot(orc)
+        ores = orc.update(grads, toks)
+        for k in range(wl.update_freq):
+            g = grads[0][k]
+            if host_inputs == "pageable":
+                src = g
+            elif host_inputs == "pinned":
+                src = torch.from_numpy(g.view(np.int16)).pin_memory()
+            else:
+                src = h2t(g)
+            if mode == "whole":
+                step.accumulate(src, toks[0][k])
+            else:
+                step.micro_begin(toks[0][k])
+                order = bucket_order(step.n_buckets) if bucket_order else range(step.n_buckets)
+                bb = step.bucket_begin
+                for b in order:
+                    step.accumulate_bucket(b, src[bb[b]:bb[b + 1]])
+        res = step.step()
+        assert decisions(res) == oracle_decisions(ores), f"update {u}: {res} vs {ores}"
+        acc = step.get_state(P.smpu.STATE_ACCUM)
+        R = ores["R"]
+        nan = np.isnan(R.view(np.float16))
+        assert np.array_equal(np.isnan(acc.view(np.float16)), nan)
+        assert np.array_equal(acc[~nan], R[~nan]), f"update {u}: accumulator differs"
+        if ores["applied"]:
+            applied += 1
+            mags.update(R, ores["e_used"], ores["N"], before["theta"], orc.theta)
+        if check_every or u == updates:
+            rtol = RTOL_1 if applied <= 1 else (rtol_last or RTOL_100)
+            check_state(gpu_state(step), snapshot(orc), mags, rtol, where=f"update {u}")
+    return step, orc
+
+
+def test_tiny_config_ten_updates_with_injected_inf(P):
+    """BASELINE configs[0]: 1M params, world=1, update_freq=2, 10 updates, +inf at (u=5, r=0, k=2, i=123457)."""
+    run_pair(P, models.tiny(), 10, rtol_last=1e-5)
+
+
+def test_tiny_hundred_updates(P):
+    wl = models.tiny(updates=100, injections=[dict(u=37, kind="NAN", r=0, k=1, i=5)])
+    run_pair(P, wl, 100, check_every=False)
+
+
+def test_first_update_within_1e6(P):
+    run_pair(P, models.tiny(injections=[]), 1)
+
+
+@pytest.mark.parametrize("kind", ["INF", "NINF", "NAN", "ACC_OVF"])
+def test_injection_kinds_skip_bitwise(P, kind):
+    inj = [dict(u=2, kind=kind, r=0, k=2, i=999_983)]
+    wl = models.Workload("inj", [("w", 1_000_000, 0)], 1, 3, injections=inj)
+    run_pair(P, wl, 3)
+
+
+def test_ragged_tensors_small_buckets_bucket_mode_out_of_order(P):
+    # odd sizes -> bucket starts not 16-aligned; tiny buckets; 3 micro-batches; buckets given in reverse order
+    tensors = [("a", 1, 0), ("b", 17, 1), ("c", 100_003, 0), ("d", 5, 1), ("e", 65_536, 2), ("f", 33, 1),
+               ("g", 250_001, 0)]
+    wl = models.Workload("ragged", tensors, 1, 3, injections=[dict(u=3, kind="INF", r=0, k=3, i=100_020)])
+    step, _ = run_pair(P, wl, 5, cfg_kw=dict(bucket_bytes=64 * 1024), mode="bucket",
+                       bucket_order=lambda nb: list(reversed(range(nb))), rtol_last=1e-5)
+    assert step.n_buckets == 3 and step.bucket_begin[1] % 16 != 0
+
+
+@pytest.mark.parametrize("host", ["pinned", "pageable"])
+def test_host_buffers(P, host):
+    wl = models.Workload("host", [("w", 40_000_001, 0), ("b", 7, 1)], 1, 2)  # > one 32 MiB staging chunk
+    run_pair(P, wl, 2, host_inputs=host)
+
+
+def test_growth_and_clamps(P):
+    # growth after 3 clean updates, max 2^9; an overflow at u=8; min clamp at 2^6
+    ocfg = O.Config(growth=3, init_scale_log2=7, max_scale_log2=9, min_scale_log2=6)
+    inj = [dict(u=8, kind="INF", r=0, k=1, i=3), dict(u=9, kind="INF", r=0, k=2, i=4),
+           dict(u=10, kind="NAN", r=0, k=1, i=5)]
+    wl = models.Workload("grow", [("w", 4096, 0), ("b", 64, 1)], 1, 2, injections=inj)
+    run_pair(P, wl, 16, ocfg=ocfg, rtol_last=1e-5)
+
+
+def test_two_x_lr_and_update_freq_1(P):
+    ocfg = O.Config(peak_lr=1e-3)   # "2x lr"
+    wl = models.Workload("c1", [("w", 300_000, 0), ("e", 70_000, 2)], 1, 1)
+    run_pair(P, wl, 4, ocfg=ocfg, rtol_last=1e-5)
+
+
+def test_bucket_size_invariance(P):
+    # buckets change timing, never values: final state bitwise equal for any bucket size
+    import torch
+    wl = models.Workload("binv", [(f"t{j}", 50_000 + 1000 * j, j % 2) for j in range(12)], 1, 2)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    finals = []
+    for bb in (2 * 60_000, 1 << 20, 150 << 20):
+        step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=bb))
+        e = 7
+        for u in range(1, 4):
+            for k in (1, 2):
+                g = h2t(synth.micro_grad_cpu(wl, lay, u, 0, k, e))
+                step.micro_begin(3000)
+                for b in range(step.n_buckets):
+                    step.accumulate_bucket(b, g[step.bucket_begin[b]:step.bucket_begin[b + 1]])
+            e = step.step()["scale_log2_next"]
+        finals.append([step.get_state(w).copy() for w in range(5)])
+        torch.cuda.synchronize()
+    for other in finals[1:]:
+        for a, b in zip(finals[0], other):
+            assert np.array_equal(a, b)
+
+
+def test_resume_bitwise(P):
+    wl = models.tiny(injections=[dict(u=4, kind="INF", r=0, k=1, i=11)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+
+    def drive(step, us):
+        for u in us:
+            e = int(step.scalars()["e"])
+            for k in (1, 2):
+                step.accumulate(h2t(synth.micro_grad_cpu(wl, lay, u, 0, k, e)), synth.ntokens(wl, u, 0, k))
+            step.step()
+
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    drive(a, range(1, 7))
+    b = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    drive(b, range(1, 4))
+    saved = [b.get_state(w).copy() for w in (0, 1, 2, 3, 5)]
+    c = P.UpdateStep(wl.numel, np.zeros(lay.n, np.float32), lib_cfg(wl))
+    for w, arr in zip((0, 1, 2, 3, 5), saved):
+        c.set_state(w, arr)
+    drive(c, range(4, 7))
+    for w in (0, 1, 2, 3, 5):
+        assert np.array_equal(a.get_state(w), c.get_state(w)), w
+
+
+def test_async_step_and_result_ring(P):
+    wl = models.Workload("async", [("w", 200_000, 0)], 1, 1)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    orc = O.Oracle(theta0)
+    ores = []
+    for u in range(1, 6):
+        g = synth.micro_grad_cpu(wl, lay, u, 0, 1, 7)
+        step.accumulate(h2t(g), 1000 + u)
+        step.step(wait=False)
+        ores.append(orc.update([[g]], [[1000 + u]]))
+    for u in range(1, 6):
+        assert decisions(step.result(u)) == oracle_decisions(ores[u - 1])
+    with pytest.raises(P.SmpuError):
+        step.result(99)
+
+
+def test_call_order_errors_and_discard(P):
+    import torch
+    wl = models.Workload("err", [("w", 1000, 0)], 1, 2)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    g = h2t(synth.micro_grad_cpu(wl, lay, 1, 0, 1, 7))
+    with pytest.raises(P.SmpuError) as ei:
+        step.step()                                    # no micro-batch yet
+    assert ei.value.status == P.smpu.ESTATE
+    step.accumulate(g, 0)
+    with pytest.raises(P.SmpuError):
+        step.accumulate_bucket(0, g)                   # no micro_begin
+    step.accumulate(g, 0)
+    with pytest.raises(P.SmpuError):
+        step.accumulate(g, 5)                          # third micro-batch with c = 2
+    before = [step.get_state(w).copy() for w in (0, 1, 2, 3, 5)]
+    with pytest.raises(P.SmpuError) as ei:
+        step.step()                                    # N = 0: discarded (reading R19)
+    assert ei.value.status == P.smpu.ESTATE
+    after = [step.get_state(w) for w in (0, 1, 2, 3, 5)]
+    for a, b in zip(before[:4], after[:4]):
+        assert np.array_equal(a, b)
+    assert after[4][:3].tolist() == before[4][:3].tolist()   # e, clean, t unchanged
+    with pytest.raises(P.SmpuError) as ei:
+        step.micro_begin(-1)
+    assert ei.value.status == P.smpu.EINVAL
+    torch.cuda.synchronize()
+
+
+class _DevF32:
+    """A device fp32 scalar owned by the library, viewed (not copied) through __cuda_array_interface__."""
+
+    def __init__(self, ptr):
+        self.__cuda_array_interface__ = {"shape": (1,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+
+def test_loss_scale_pointer_tracks_scaler(P):
+    import torch
+    wl = models.Workload("ls", [("w", 4096, 0)], 1, 1, injections=[dict(u=2, kind="INF", r=0, k=1, i=0)])
+    lay = synth.Layout(wl)
+    step = P.UpdateStep(wl.numel, synth.theta0_cpu(wl, lay), lib_cfg(wl))
+    scale = torch.as_tensor(_DevF32(step.loss_scale_ptr()), device="cuda")
+    assert scale.item() == 2.0 ** 7
+    for u in (1, 2):
+        step.accumulate(h2t(synth.micro_grad_cpu(wl, lay, u, 0, 1, 7)), 100)
+        res = step.step()
+        assert scale.item() == 2.0 ** res["scale_log2_next"]
+    assert res["overflow"] == 1 and scale.item() == 2.0 ** 6
