@@ -228,17 +228,18 @@ def main_ours(args):
         if world > 1:
             dist.barrier()
 
+    t_w = time.perf_counter()
     for _ in range(args.warmup):
         one_update()
     torch.cuda.synchronize()
+    per_update = _max_over_ranks((time.perf_counter() - t_w) / max(1, args.warmup), world)
+    soak = max(2, min(2000, int(0.6 / max(per_update, 1e-5))))     # same count on every rank (NCCL)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         # soak under the same load for ~0.6 s so that the 100 ms clock sampler sees the timed region's state
-        t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 0.6:
+        for _ in range(soak):
             one_update()
-            torch.cuda.synchronize()
         step.kernel_stats(reset=True)
         step.set_timing(True)
         torch.cuda.synchronize()
