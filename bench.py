@@ -256,6 +256,29 @@ def main_ours(args):
     last = step.result(step.scalars()["attempts"])
     assert last["applied"] == 1 and last["overflow"] == 0, last
 
+    # ---- exposed communication: the same per-GPU work through a world = 1 ctx on the same GPU
+    exposed = None
+    if world > 1:
+        step1 = P.UpdateStep(wl.numel, theta0, cfg, world=1, rank=0, device=local)
+
+        def one_update1():
+            for k in range(c):
+                step1.accumulate(grads[k], toks[k], stream)
+            step1.step(stream, wait=False)
+        for _ in range(args.warmup):
+            one_update1()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_update1()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t1 = _max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        step1.close()
+        del step1
+        exposed = t1
+
     # ---- end-to-end through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -293,8 +316,9 @@ def main_ours(args):
     peak_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "of fallback (B200_PROFILING.md)"
     nb = step.n_buckets
     # algorithmic bytes per launch: K1 first 4 B/elem, K1 add 6, K1s 2, K2 28
-    per_elem = {"k1_first": 4, "k1_add": 6, "k1s_sweep": 2, "k2_adam": 28}
-    elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n, "k1s_sweep": n if world > 1 else 0, "k2_adam": n}
+    # (K1s only sweeps when the early decision was undecided; with G_real it returns at once)
+    per_elem = {"k1_first": 4, "k1_add": 6, "k2_adam": 28}
+    elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n, "k2_adam": n}
     kernels = {}
     for k, bpe in per_elem.items():
         st = kstat[k]
@@ -310,7 +334,7 @@ def main_ours(args):
     roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["achieved_gbs"], "peak": hbm_peak,
             "unit": "GB/s", "frac": kernels[dom]["achieved_gbs"] / hbm_peak, "peak_source": peak_src,
             "traffic": traffic}
-    path_bytes = n * (6 * c - 2 + 28 + (2 if world > 1 else 0))
+    path_bytes = n * (6 * c - 2 + 28)
     out = {"metric": METRIC, "value": world * c * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f16+f32", "data": "synthetic",
@@ -325,6 +349,10 @@ def main_ours(args):
            "gpu_launches": int(sum(kstat[k]["launches"] for k in ("k1_first", "k1_add", "k1s_sweep", "k0_decide",
                                                                    "k2_adam"))),
            "clocks": clk.summary()}
+    if exposed is not None:
+        out["exposed_comm"] = {"ms": ms - exposed, "frac_of_update": (ms - exposed) / ms, "t_world1_ms": exposed,
+                               "method": "T(update, W ranks) - T(same per-GPU work through a world=1 ctx, same "
+                                         "GPU, same run); library-only step (no backward to hide behind)"}
     if world > 1 and kstat["nccl_allreduce"]["ms"] > 0:
         ar_ms = kstat["nccl_allreduce"]["ms"] / args.steps
         bus = 2 * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9

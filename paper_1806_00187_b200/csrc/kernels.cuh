@@ -2,11 +2,14 @@
 //
 //   K1   accumulate   A = g (first micro-batch) | A = rn16(A + g) (later ones), optional overflow test of
 //                     the OUTPUT A (finite + finite can overflow: 65504 + 16 -> inf).
-//   K1s  sweep        overflow test of the reduced bucket R after its all-reduce (W > 1).    P:158, reading R4
-//   K0   decide       one thread: flag -> skip/apply, dynamic loss scaler, t, lr(t), Adam scalars, result
-//                     record, next loss scale.
-//   K2   adam         fused unscale + normalise by N + Adam (fp32 master) + fp16 re-cast; every CTA exits
-//                     before any store when K0 decided to skip.
+//   K1s  sweep        overflow test of the reduced R, W > 1, only when the early decision was undecided.  P:158, R4
+//   K0   decide       one thread: overflow -> skip/apply, dynamic loss scaler, t, lr(t), Adam scalars, result
+//                     record, next loss scale.  W = 1: from K1's flag.  W > 1: EARLY from an all-reduced
+//                     (N, sum_r max|A_r|) pair before the gradient all-reduces finish (exact, see k0_early),
+//                     LATE from the K1s sweep in the rare undecided case.
+//   K2   adam         fused unscale + normalise by N + Adam (fp32 master) + fp16 re-cast, per bucket right
+//                     behind that bucket's all-reduce (W > 1) or whole (W = 1); every CTA exits before any
+//                     store when K0 decided to skip.
 //   Kc   cast         w16 = rn16(theta) (init / set_state only).
 //
 // All of them are HBM-streaming: 256-bit (v8.b32) global accesses (sm_100a LDG/STG.256), L1 no-allocate,
@@ -76,12 +79,24 @@ __device__ __forceinline__ void raise_flag(bool bad, int* flag) {
     if (any && (threadIdx.x & 31) == (unsigned)(__ffs(any) - 1)) *(volatile int*)flag = 1;
 }
 
+// max of the fp16 magnitudes (bits & 0x7FFF, monotone in |x|; >= 0x7C00 iff non-finite) of a packed word
+__device__ __forceinline__ uint32_t mag_max2(uint32_t m, uint32_t w) { return __vmaxu2(m, w & 0x7FFF7FFFu); }
+
+__device__ __forceinline__ void publish_max(uint32_t m2, uint32_t* stat) {
+    uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(stat, m);
+}
+
 // ---------------------------------------------------------------------------------------------- K1
 // acc[lo, hi) (absolute indices) <- g[0, hi-lo) (+ acc).  Vector path when acc+i and g+(i-lo) are
 // both 32-B aligned at the first 16-element boundary i >= lo, else an element path (correct, slower).
-template <bool FIRST, bool DETECT>
+// DETECT: flag |= any non-finite output (W = 1 last micro-batch).  STATS: *stat = max(*stat, max fp16
+// magnitude bits of the output) (W > 1 last micro-batch: input of the early overflow decision, K0 EARLY).
+template <bool FIRST, bool DETECT, bool STATS = false>
 __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc, const uint16_t* __restrict__ g,
-                                                     int64_t lo, int64_t hi, int* __restrict__ flag) {
+                                                     int64_t lo, int64_t hi, int* __restrict__ flag,
+                                                     uint32_t* __restrict__ stat = nullptr) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const uint16_t* gb = g - lo;                       // gb[i] is the gradient of element i
@@ -90,7 +105,7 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
     bool vec_ok = ((reinterpret_cast<uintptr_t>(gb + vbeg) & 31) == 0);
     int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
     int64_t vend = vbeg + nvec * 16;
-    uint32_t bad = 0;
+    uint32_t bad = 0, mx = 0;
     if (vec_ok) {
         // body: 16 halves per unit, two units per thread in flight
         int64_t u = tid;
@@ -105,6 +120,10 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
             if (DETECT) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(g0.w[j]) | nonfinite_bits(g1.w[j]);
+            }
+            if (STATS) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx = mag_max2(mag_max2(mx, g0.w[j]), g1.w[j]);
             }
             st256(acc + i0, g0);
             st256(acc + i1, g1);
@@ -121,6 +140,10 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(g0.w[j]);
             }
+            if (STATS) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx = mag_max2(mx, g0.w[j]);
+            }
             st256(acc + i0, g0);
         }
     }
@@ -132,6 +155,7 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
             x = (uint16_t)(s & 0xFFFFu);
         }
         if (DETECT && h_nonfinite(x)) bad |= 1u;
+        if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
         acc[i] = x;
     };
     if (vec_ok) {
@@ -141,11 +165,17 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
         for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
     }
     if (DETECT) raise_flag(bad != 0, flag);
+    if (STATS) publish_max(mx, stat);
 }
 
 // ---------------------------------------------------------------------------------------------- K1s
+struct Scalars;
+__device__ __forceinline__ int32_t decision_of(const Scalars* sc);
+
+// only when the early decision could not decide (K0 EARLY wrote UNDECIDED); otherwise returns at once
 __global__ void __launch_bounds__(256) k1s_sweep(const uint16_t* __restrict__ R, int64_t lo, int64_t hi,
-                                                 int* __restrict__ flag) {
+                                                 int* __restrict__ flag, const Scalars* __restrict__ sc) {
+    if (decision_of(sc) != 2) return;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     int64_t vbeg = (lo + 15) & ~(int64_t)15;
@@ -176,13 +206,18 @@ struct DevState {          // device-resident scaler / optimizer counters
     int64_t attempts;      // update attempts
 };
 
+// decision states (Scalars::state)
+enum : int32_t { DEC_APPLY = 0, DEC_SKIP = 1, DEC_UNDECIDED = 2, DEC_APPLY_LATE = 3 };
+
 struct Scalars {           // written by K0, read by every K2 CTA
-    int32_t skip;
+    int32_t state;         // DEC_*
     float inv_sN;          // fp32(1 / (2^e * N))
     float step;            // fp32(lr / bc1)
     float inv_sqrt_bc2;    // fp32(1 / sqrt(bc2))
     float b1, omb1, b2, omb2, eps;
 };
+
+__device__ __forceinline__ int32_t decision_of(const Scalars* sc) { return *(volatile const int32_t*)&sc->state; }
 
 struct DevCfg {
     double peak_lr;
@@ -202,14 +237,10 @@ __device__ __forceinline__ float lr_at(int64_t t, const DevCfg& c) {
     return __double2float_rn(__dmul_rn(c.peak_lr, f));
 }
 
-__global__ void k0_decide(int* __restrict__ flag, const int64_t* __restrict__ dev_tokens, int64_t local_tokens,
-                          int use_dev_tokens, DevState* __restrict__ st, Scalars* __restrict__ sc,
-                          float* __restrict__ loss_scale, smpu_step_result* __restrict__ ring, int ring_mask,
-                          DevCfg cfg) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int overflow = *(volatile int*)flag != 0;
-    *(volatile int*)flag = 0;                          // re-armed for the next update
-    const int64_t N = use_dev_tokens ? *dev_tokens : local_tokens;
+// The scaler step + Adam scalars + result record, once per update attempt.
+// Returns the decision state written (DEC_APPLY / DEC_SKIP; apply_state for a late decision).
+__device__ void decide(int overflow, int64_t N, DevState* st, Scalars* sc, float* loss_scale,
+                       smpu_step_result* ring, int ring_mask, const DevCfg& cfg, int32_t apply_state) {
     DevState s = *st;
     smpu_step_result r;
     r.attempt = ++s.attempts;
@@ -217,20 +248,20 @@ __global__ void k0_decide(int* __restrict__ flag, const int64_t* __restrict__ de
     r.scale_log2_used = (int32_t)s.e;
     r.ntokens_total = N;
     r.discarded = 0;
-    int skip;
+    int32_t state;
     if (N <= 0) {                                      // reading R19: nothing changes
-        skip = 1;
+        state = DEC_SKIP;
         r.discarded = 1;
         r.applied = 0;
         r.lr = lr_at(s.t + 1, cfg);
     } else if (overflow) {                             // P:158 "scales down the loss when overflow is detected"
-        skip = 1;
+        state = DEC_SKIP;
         s.e = s.e - 1 < cfg.emin ? cfg.emin : s.e - 1;
         s.clean = 0;
         r.applied = 0;
         r.lr = lr_at(s.t + 1, cfg);                    // reading R15
     } else {
-        skip = 0;
+        state = apply_state;
         s.t += 1;
         s.clean += 1;
         r.applied = 1;
@@ -252,7 +283,7 @@ __global__ void k0_decide(int* __restrict__ flag, const int64_t* __restrict__ de
             s.clean = 0;
         }
     }
-    sc->skip = skip;
+    sc->state = state;
     r.scale_log2_next = (int32_t)s.e;
     r.num_updates = s.t;
     r.clean_streak = s.clean;
@@ -260,6 +291,59 @@ __global__ void k0_decide(int* __restrict__ flag, const int64_t* __restrict__ de
     *loss_scale = ldexpf(1.0f, (int)s.e);
     ring[(r.attempt - 1) & ring_mask] = r;             // mapped pinned host memory
     __threadfence_system();
+}
+
+// W = 1: the last K1 tested the reduced (= local) gradient exactly.
+__global__ void k0_decide(int* __restrict__ flag, int64_t tokens, DevState* __restrict__ st, Scalars* __restrict__ sc,
+                          float* __restrict__ loss_scale, smpu_step_result* __restrict__ ring, int ring_mask,
+                          DevCfg cfg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int overflow = *(volatile int*)flag != 0;
+    *(volatile int*)flag = 0;                          // re-armed for the next update
+    decide(overflow, tokens, st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY);
+}
+
+// W > 1, before the gradient all-reduces finish.  xs = {N, sum_r M_r} summed over ranks by one int64
+// all-reduce, M_r = rank r's max |A_r| in units of 2^-24 (or kNonFinite if A_r holds inf/NaN).
+//   some A_r non-finite            => R non-finite in every order            => overflow (exact)
+//   sum_r M_r <= 2^15 (all finite) => every partial sum of any order and width stays < 65520 (W-1 roundings
+//                                     add at most 16 each) => R finite       => clean (exact)
+//   otherwise                      => UNDECIDED: the sweep of R (K1s) and K0 LATE decide after the reduce.
+// Overflow <=> "R holds a non-finite element" (reading R4) holds in all three cases.
+constexpr int64_t kNonFinite = int64_t(1) << 50;   // > 1024 ranks x 2^40 (65504 in units of 2^-24)
+__device__ __forceinline__ int64_t mag_units(uint32_t bits) {
+    if (bits >= 0x7C00u) return kNonFinite;
+    int ex = (int)(bits >> 10), man = (int)(bits & 0x3FF);
+    return ex == 0 ? (int64_t)man : ((int64_t)(1024 + man)) << (ex - 1);   // |x| / 2^-24
+}
+
+__global__ void k_stats_prep(uint32_t* __restrict__ stat, int64_t local_tokens, int64_t* __restrict__ xs) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    xs[0] = local_tokens;
+    xs[1] = mag_units(*stat);
+    *stat = 0;                                         // re-armed for the next update
+}
+
+__global__ void k0_early(const int64_t* __restrict__ xs, DevState* __restrict__ st, Scalars* __restrict__ sc,
+                         float* __restrict__ loss_scale, smpu_step_result* __restrict__ ring, int ring_mask,
+                         DevCfg cfg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t N = xs[0], M = xs[1];
+    if (M >= kNonFinite) decide(1, N, st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY);
+    else if (M <= (int64_t(1) << 39)) decide(0, N, st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY);
+    else sc->state = DEC_UNDECIDED;                    // 2^39 units = 2^15
+}
+
+// W > 1, after every all-reduce and (if undecided) the K1s sweeps.
+__global__ void k0_late(int* __restrict__ flag, const int64_t* __restrict__ xs, DevState* __restrict__ st,
+                        Scalars* __restrict__ sc, float* __restrict__ loss_scale, smpu_step_result* __restrict__ ring,
+                        int ring_mask, DevCfg cfg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (sc->state == DEC_UNDECIDED) {
+        const int overflow = *(volatile int*)flag != 0;
+        decide(overflow, xs[0], st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY_LATE);
+    }
+    *(volatile int*)flag = 0;
 }
 
 // ---------------------------------------------------------------------------------------------- K2
@@ -295,18 +379,24 @@ __device__ __forceinline__ void adam_unit(const V4& r16, V8& th, V8& m, V8& v, V
     }
 }
 
+// Elements [lo, hi) of the ctx arrays (a bucket, or everything).  Runs only when K0 wrote `need`
+// (DEC_APPLY for the exact early / W = 1 decision, DEC_APPLY_LATE for the fallback); on a skip every CTA
+// returns before any store (R6).  Vector units of 8 elements start at the first multiple of 8 >= lo
+// (the arrays are 256-B aligned), head and tail take the element path.
 __global__ void __launch_bounds__(256) k2_adam(float* __restrict__ theta, float* __restrict__ m,
                                                float* __restrict__ v, uint16_t* __restrict__ w16,
-                                               const uint16_t* __restrict__ R, int64_t n,
-                                               const Scalars* __restrict__ scp) {
-    if (*(volatile const int32_t*)&scp->skip) return;  // skipped update: no store at all (R6)
+                                               const uint16_t* __restrict__ R, int64_t lo, int64_t hi,
+                                               const Scalars* __restrict__ scp, int32_t need) {
+    if (decision_of(scp) != need) return;
     const Scalars s = *scp;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-    const int64_t nvec = n / 8;                        // 8 elements per unit
+    int64_t vbeg = (lo + 7) & ~(int64_t)7;
+    if (vbeg > hi) vbeg = hi;
+    const int64_t nvec = (hi - vbeg) / 8, vend = vbeg + nvec * 8;
     int64_t u = tid;
     for (; u + nthr < nvec; u += 2 * nthr) {
-        const int64_t i0 = u * 8, i1 = (u + nthr) * 8;
+        const int64_t i0 = vbeg + u * 8, i1 = vbeg + (u + nthr) * 8;
         V4 r0 = ld128_ro(R + i0), r1 = ld128_ro(R + i1);
         V8 t0 = ld256(theta + i0), t1 = ld256(theta + i1);
         V8 m0 = ld256(m + i0), m1 = ld256(m + i1);
@@ -324,7 +414,7 @@ __global__ void __launch_bounds__(256) k2_adam(float* __restrict__ theta, float*
         st128(w16 + i1, w1);
     }
     if (u < nvec) {
-        const int64_t i0 = u * 8;
+        const int64_t i0 = vbeg + u * 8;
         V4 r0 = ld128_ro(R + i0);
         V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
         V4 w0;
@@ -334,14 +424,16 @@ __global__ void __launch_bounds__(256) k2_adam(float* __restrict__ theta, float*
         st256(v + i0, v0);
         st128(w16 + i0, w0);
     }
-    for (int64_t i = nvec * 8 + tid; i < n; i += nthr) {
+    auto elem = [&](int64_t i) {
         float th = theta[i], mm = m[i], vv = v[i];
         adam_elem(__half2float(__ushort_as_half(R[i])), th, mm, vv, s);
         theta[i] = th;
         m[i] = mm;
         v[i] = vv;
         w16[i] = __half_as_ushort(__float2half_rn(th));
-    }
+    };
+    for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+    for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
 }
 
 // ---------------------------------------------------------------------------------------------- Kc
@@ -350,7 +442,5 @@ __global__ void kc_cast(const float* __restrict__ theta, uint16_t* __restrict__ 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr)
         w16[i] = __half_as_ushort(__float2half_rn(theta[i]));
 }
-
-__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
 
 }  // namespace smpu

@@ -4,13 +4,16 @@
 //   theta fp32[n], m fp32[n], v fp32[n]       fp32 master weights + Adam moments
 //   w16   fp16[n]                             fp16 model weights, re-cast each update
 //   acc   fp16[n]                             accumulator; buckets are views of it
-//   flag int32, tokens int64, DevState, Scalars, loss scale fp32   (device scalars; K0 owns them)
+//   flag int32, stat u32, xs int64[2], DevState, Scalars, loss scale fp32   (device scalars; K0 owns them)
 //   result ring: 64 smpu_step_result in mapped pinned host memory (written by K0).
 //
-// Streams: K1 runs on the caller's stream; per-bucket NCCL all-reduce + K1s run on a high-priority
-// comm stream gated by one ready event per bucket (the paper's "background thread", becomes a
-// stream: enqueue is already asynchronous); K0 + K2 run on the stream given to smpu_step after it waits
-// for the comm stream.  No host synchronisation anywhere on the update path.
+// Streams (W > 1): K1 runs on the caller's stream; each bucket's NCCL all-reduce runs on a high-priority
+// comm stream gated by that bucket's ready event (the paper's "background thread", becomes a stream:
+// enqueue is already asynchronous); once the last micro-batch is accumulated, a decision stream all-reduces
+// 16 bytes (N and sum_r max|A_r|) on a second communicator and K0 EARLY decides overflow exactly in the
+// common case; a K2 stream then runs Adam on bucket b as soon as bucket b's all-reduce lands, overlapping
+// the remaining all-reduces.  smpu_step enqueues only the (normally empty) fallback.  W = 1: K1 -> K0 -> K2 on
+// the caller's streams.  No host synchronisation anywhere on the update path.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -55,7 +58,8 @@ struct smpu_ctx {
     float *theta = nullptr, *m = nullptr, *v = nullptr;
     uint16_t *w16 = nullptr, *acc = nullptr;
     int* flag = nullptr;
-    int64_t* tokens = nullptr;
+    uint32_t* stat = nullptr;      // local max fp16 magnitude bits of the last micro-batch's output (W > 1)
+    int64_t* xs = nullptr;         // {N_r, M_r} -> all-reduced {N, sum_r M_r} (W > 1)
     DevState* st = nullptr;
     Scalars* sc = nullptr;
     float* scale = nullptr;
@@ -64,10 +68,11 @@ struct smpu_ctx {
     cudaEvent_t ring_ev[kRing] = {};
     DevCfg dcfg{};
 
-    ncclComm_t comm = nullptr;
-    cudaStream_t comm_stream = nullptr, copy_stream = nullptr;
-    std::vector<cudaEvent_t> ready;
-    cudaEvent_t comm_done = nullptr, order_ev = nullptr;
+    ncclComm_t comm = nullptr;     // gradient buckets
+    ncclComm_t comm2 = nullptr;    // the 16-byte decision all-reduce, concurrent with the bucket all-reduces
+    cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
+    std::vector<cudaEvent_t> ready, ar_done;
+    cudaEvent_t comm_done = nullptr, order_ev = nullptr, dec_ev = nullptr, k2_done = nullptr;
     cudaStream_t last_stream = nullptr;
     bool have_order = false;
 
@@ -185,11 +190,14 @@ int grid_for(int64_t units, int max_grid) {
 }
 
 smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, bool first, bool detect,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool stats = false) {
     if (hi <= lo) return SMPU_OK;
     int grid = grid_for((hi - lo + 15) / 16, ctx->grid_k1);
     Timed t(ctx, first ? SMPU_K1_FIRST : SMPU_K1_ADD, s);
-    if (first) {
+    if (stats) {
+        if (first) k1_accumulate<true, false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag, ctx->stat);
+        else k1_accumulate<false, false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag, ctx->stat);
+    } else if (first) {
         if (detect) k1_accumulate<true, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
         else k1_accumulate<true, false><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
     } else {
@@ -202,8 +210,8 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
 
 // accumulate src (host or device) into acc[lo, hi)
 smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, bool first, bool detect,
-                             cudaStream_t s) {
-    if (classify(src) == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s);
+                             cudaStream_t s, bool stats = false) {
+    if (classify(src) == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s, stats);
     // host memory: double-buffered H2D staging on the copy stream, overlapped with K1 on `s`
     for (int64_t c0 = lo; c0 < hi; c0 += kStageElems) {
         int64_t c1 = c0 + kStageElems < hi ? c0 + kStageElems : hi;
@@ -214,7 +222,7 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
         CK(cudaEventRecord(ctx->stage_full[j], ctx->copy_stream));
         CK(cudaStreamWaitEvent(s, ctx->stage_full[j], 0));
         // the staging buffer holds elements [c0, c1): index it relative to c0
-        smpu_status st = launch_k1(ctx, ctx->stage[j], c0, c1, first, detect, s);
+        smpu_status st = launch_k1(ctx, ctx->stage[j], c0, c1, first, detect, s, stats);
         if (st != SMPU_OK) return st;
         CK(cudaEventRecord(ctx->stage_free[j], s));
     }
@@ -228,23 +236,45 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
         int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
         cudaStream_t cs = ctx->comm_stream;
         CK(cudaStreamWaitEvent(cs, ctx->ready[b], 0));
-        if (b == 0) {   // global token count N = sum_r N_r, issued with the first bucket
-            k_set_i64<<<1, 1, 0, cs>>>(ctx->tokens, ctx->local_tokens);
-            CKL("k_set_i64");
-            NK(ncclAllReduce(ctx->tokens, ctx->tokens, 1, ncclInt64, ncclSum, ctx->comm, cs));
-        }
         {
             Timed t(ctx, SMPU_NCCL_AR, cs);
             NK(ncclAllReduce(ctx->acc + lo, ctx->acc + lo, (size_t)(hi - lo), ncclFloat16, ncclSum, ctx->comm, cs));
         }
-        {
-            Timed t(ctx, SMPU_K1S, cs);
-            k1s_sweep<<<grid_for((hi - lo + 15) / 16, ctx->grid_k1s), 256, 0, cs>>>(ctx->acc, lo, hi, ctx->flag);
-            CKL("k1s_sweep");
-        }
+        CK(cudaEventRecord(ctx->ar_done[b], cs));
         ctx->next_issue++;
     }
     if (ctx->next_issue == ctx->nb) CK(cudaEventRecord(ctx->comm_done, ctx->comm_stream));
+    return SMPU_OK;
+}
+
+// W > 1, once every bucket of the last micro-batch is accumulated: the exact early overflow decision
+// (k0_early) from one 16-byte all-reduce on a second communicator, then Adam per bucket on its own stream,
+// each bucket right behind its gradient all-reduce -- K2 overlaps the remaining all-reduces.
+smpu_status issue_decision(smpu_ctx* ctx) {
+    cudaStream_t ds = ctx->dec_stream, ks = ctx->k2_stream;
+    for (int b = 0; b < ctx->nb; ++b) CK(cudaStreamWaitEvent(ds, ctx->ready[b], 0));
+    {
+        Timed t(ctx, SMPU_K0, ds);
+        k_stats_prep<<<1, 32, 0, ds>>>(ctx->stat, ctx->local_tokens, ctx->xs);
+        CKL("k_stats_prep");
+    }
+    NK(ncclAllReduce(ctx->xs, ctx->xs, 2, ncclInt64, ncclSum, ctx->comm2, ds));   // N and sum_r M_r
+    {
+        Timed t(ctx, SMPU_K0, ds);
+        k0_early<<<1, 32, 0, ds>>>(ctx->xs, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg);
+        CKL("k0_early");
+    }
+    CK(cudaEventRecord(ctx->dec_ev, ds));
+    CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
+    for (int b = 0; b < ctx->nb; ++b) {
+        int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
+        CK(cudaStreamWaitEvent(ks, ctx->ar_done[b], 0));
+        Timed t(ctx, SMPU_K2, ks);
+        k2_adam<<<grid_for((hi - lo + 7) / 8, ctx->grid_k2), 256, 0, ks>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
+                                                                           ctx->acc, lo, hi, ctx->sc, DEC_APPLY);
+        CKL("k2_adam");
+    }
+    CK(cudaEventRecord(ctx->k2_done, ks));
     return SMPU_OK;
 }
 
@@ -283,6 +313,7 @@ void free_ctx(smpu_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->dev);
     cudaDeviceSynchronize();
+    if (c->comm2) ncclCommDestroy(c->comm2);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->theta);
     cudaFree(c->m);
@@ -290,7 +321,8 @@ void free_ctx(smpu_ctx* c) {
     cudaFree(c->w16);
     cudaFree(c->acc);
     cudaFree(c->flag);
-    cudaFree(c->tokens);
+    cudaFree(c->stat);
+    cudaFree(c->xs);
     cudaFree(c->st);
     cudaFree(c->sc);
     cudaFree(c->scale);
@@ -299,6 +331,11 @@ void free_ctx(smpu_ctx* c) {
     if (c->ring_host) cudaFreeHost(c->ring_host);
     for (auto& e : c->ring_ev) if (e) cudaEventDestroy(e);
     for (auto& e : c->ready) if (e) cudaEventDestroy(e);
+    for (auto& e : c->ar_done) if (e) cudaEventDestroy(e);
+    if (c->dec_ev) cudaEventDestroy(c->dec_ev);
+    if (c->k2_done) cudaEventDestroy(c->k2_done);
+    if (c->dec_stream) cudaStreamDestroy(c->dec_stream);
+    if (c->k2_stream) cudaStreamDestroy(c->k2_stream);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (int j = 0; j < 2; ++j) {
         if (c->stage_free[j]) cudaEventDestroy(c->stage_free[j]);
@@ -414,7 +451,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMalloc(&ctx->w16, n * 2));
     IK(cudaMalloc(&ctx->acc, n * 2));
     IK(cudaMalloc(&ctx->flag, sizeof(int)));
-    IK(cudaMalloc(&ctx->tokens, sizeof(int64_t)));
+    IK(cudaMalloc(&ctx->stat, sizeof(uint32_t)));
+    IK(cudaMalloc(&ctx->xs, 2 * sizeof(int64_t)));
     IK(cudaMalloc(&ctx->st, sizeof(DevState)));
     IK(cudaMalloc(&ctx->sc, sizeof(Scalars)));
     IK(cudaMalloc(&ctx->scale, sizeof(float)));
@@ -426,6 +464,10 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     for (auto& e : ctx->ring_ev) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->ready.resize(ctx->nb);
     for (auto& e : ctx->ready) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ar_done.resize(ctx->nb);
+    for (auto& e : ctx->ar_done) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    IK(cudaEventCreateWithFlags(&ctx->dec_ev, cudaEventDisableTiming));
+    IK(cudaEventCreateWithFlags(&ctx->k2_done, cudaEventDisableTiming));
     ctx->bucket_done.assign(ctx->nb, 0);
     IK(cudaEventCreateWithFlags(&ctx->comm_done, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming));
@@ -433,6 +475,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     IK(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio));
     IK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    IK(cudaStreamCreateWithPriority(&ctx->dec_stream, cudaStreamNonBlocking, hi_prio));
+    IK(cudaStreamCreateWithFlags(&ctx->k2_stream, cudaStreamNonBlocking));
     for (int j = 0; j < 2; ++j) {
         IK(cudaEventCreateWithFlags(&ctx->stage_free[j], cudaEventDisableTiming));
         IK(cudaEventCreateWithFlags(&ctx->stage_full[j], cudaEventDisableTiming));
@@ -464,7 +508,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMemsetAsync(ctx->v, 0, n * 4, s0));
     IK(cudaMemsetAsync(ctx->acc, 0, n * 2, s0));
     IK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), s0));
-    IK(cudaMemsetAsync(ctx->tokens, 0, sizeof(int64_t), s0));
+    IK(cudaMemsetAsync(ctx->stat, 0, sizeof(uint32_t), s0));
+    IK(cudaMemsetAsync(ctx->xs, 0, 2 * sizeof(int64_t), s0));
     IK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), s0));
     DevState st0{cfg->init_scale_log2, 0, 0, 0};
     IK(cudaMemcpyAsync(ctx->st, &st0, sizeof st0, cudaMemcpyHostToDevice, s0));
@@ -480,6 +525,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         // replicas start bitwise identical: rank 0's theta_0
         r = ncclBroadcast(ctx->theta, ctx->theta, (size_t)n, ncclFloat32, 0, ctx->comm, s0);
         if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclBroadcast", __LINE__));
+        r = ncclCommSplit(ctx->comm, 0, rank, &ctx->comm2, nullptr);
+        if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclCommSplit", __LINE__));
     }
     kc_cast<<<grid_for(n, ctx->grid_k2), 256, 0, s0>>>(ctx->theta, ctx->w16, n);
     ctx->launches[SMPU_KCAST]++;
@@ -541,18 +588,22 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
     if (st != SMPU_OK) return st;
     const bool last = final_micro(ctx);
     const bool first = ctx->micro == 1;
+    const bool multi = last && ctx->world > 1;
     st = accumulate_range(ctx, (const uint16_t*)grads, ctx->bbegin[bucket], ctx->bbegin[bucket + 1], first,
-                          last && ctx->world == 1, s);
+                          last && ctx->world == 1, s, multi);
     if (st != SMPU_OK) return st;
     ctx->bucket_done[bucket] = 1;
-    if (last && ctx->world > 1) {
+    if (multi) {
         CK(cudaEventRecord(ctx->ready[bucket], s));
         st = issue_ready_buckets(ctx);
         if (st != SMPU_OK) return st;
     }
     st = leave_stream(ctx, s);
     if (st != SMPU_OK) return st;
-    if (--ctx->buckets_left == 0) ctx->bucket_micro = false;
+    if (--ctx->buckets_left == 0) {
+        ctx->bucket_micro = false;
+        if (multi) return issue_decision(ctx);
+    }
     return SMPU_OK;
 }
 
@@ -607,18 +658,42 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     cudaStream_t s = (cudaStream_t)stream;
     smpu_status st = enter_stream(ctx, s);
     if (st != SMPU_OK) return st;
-    if (ctx->world > 1) CK(cudaStreamWaitEvent(s, ctx->comm_done, 0));
-    {
-        Timed t(ctx, SMPU_K0, s);
-        k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->tokens, ctx->local_tokens, ctx->world > 1, ctx->st, ctx->sc,
-                                   ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg);
-        CKL("k0_decide");
-    }
-    {
-        Timed t(ctx, SMPU_K2, s);
-        k2_adam<<<grid_for((ctx->n + 7) / 8, ctx->grid_k2), 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
-                                                                         ctx->acc, ctx->n, ctx->sc);
-        CKL("k2_adam");
+    if (ctx->world > 1) {
+        // the exact early decision and the per-bucket Adam are already enqueued (issue_decision); here only
+        // the fallback for the rare undecided case: sweep R, decide, Adam on everything.  All three kernels
+        // return at once when K0 EARLY decided.
+        CK(cudaStreamWaitEvent(s, ctx->comm_done, 0));
+        CK(cudaStreamWaitEvent(s, ctx->k2_done, 0));
+        {
+            Timed t(ctx, SMPU_K1S, s);
+            k1s_sweep<<<ctx->grid_k1s, 256, 0, s>>>(ctx->acc, 0, ctx->n, ctx->flag, ctx->sc);
+            CKL("k1s_sweep");
+        }
+        {
+            Timed t(ctx, SMPU_K0, s);
+            k0_late<<<1, 32, 0, s>>>(ctx->flag, ctx->xs, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1,
+                                     ctx->dcfg);
+            CKL("k0_late");
+        }
+        {
+            Timed t(ctx, SMPU_K2, s);
+            k2_adam<<<ctx->grid_k2, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, 0, ctx->n, ctx->sc,
+                                                 DEC_APPLY_LATE);
+            CKL("k2_adam");
+        }
+    } else {
+        {
+            Timed t(ctx, SMPU_K0, s);
+            k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->local_tokens, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev,
+                                       kRing - 1, ctx->dcfg);
+            CKL("k0_decide");
+        }
+        {
+            Timed t(ctx, SMPU_K2, s);
+            k2_adam<<<grid_for((ctx->n + 7) / 8, ctx->grid_k2), 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
+                                                                             ctx->acc, 0, ctx->n, ctx->sc, DEC_APPLY);
+            CKL("k2_adam");
+        }
     }
     ctx->attempts++;
     CK(cudaEventRecord(ctx->ring_ev[(ctx->attempts - 1) % kRing], s));

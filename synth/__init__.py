@@ -16,7 +16,7 @@ from .models import WORKLOADS, Workload, base_ende, big_ende, big_enfr, tiny, tr
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 FAMILIES = {"real": 0, "exact": 1, "zero": 2}
-INF16, NINF16, NAN16, MAX16, R40000 = 0x7C00, 0xFC00, 0x7E00, 0x7BFF, 0x78E2
+INF16, NINF16, NAN16, MAX16, R40000, R20000 = 0x7C00, 0xFC00, 0x7E00, 0x7BFF, 0x78E2, 0x74E2
 
 _lib = None
 _glib = None
@@ -102,7 +102,9 @@ def overrides(wl: Workload, u: int, r: int, k: int):
     INF/NINF/NAN write the pattern at (u, r, k, i).  ACC_OVF: 65504 at k=1,2 on rank r,
     every other contribution at i zero (overflow by local accumulation).  RED_OVF:
     40000 at k=c on every rank, every other contribution at i zero (overflow only after
-    the cross-rank sum; needs W >= 2)."""
+    the cross-rank sum; needs W >= 2).  BIG: 20000 at k=c on ranks 0 and 1, every other contribution at i
+    zero (a finite 40000 after the sum, large enough that the early decision of the W > 1 path must defer
+    to the sweep of R)."""
     out = []
     c, W = wl.update_freq, wl.world
     for inj in wl.injections:
@@ -120,6 +122,10 @@ def overrides(wl: Workload, u: int, r: int, k: int):
             if W < 2:
                 raise ValueError("RED_OVF needs world >= 2")
             out.append((i, R40000 if k == c else 0))
+        elif kind == "BIG":
+            if W < 2:
+                raise ValueError("BIG needs world >= 2")
+            out.append((i, R20000 if (k == c and r < 2) else 0))
         else:
             raise ValueError(kind)
     return out

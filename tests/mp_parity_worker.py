@@ -27,15 +27,17 @@ from tests.gpu_util import (RTOL_1, Magnitudes, check_state, decisions, gpu_stat
 
 def main():
     family = sys.argv[1] if len(sys.argv) > 1 else "exact"
-    updates = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    updates = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = 3
     tensors = [("w0", 300_001, 0), ("b0", 1025, 1), ("w1", 262_144, 0), ("e", 131_072, 2), ("b1", 7, 1)]
-    inj = [dict(u=3, kind="RED_OVF", i=262_150), dict(u=5, kind="INF", r=world - 1, k=2, i=17),
-           dict(u=6, kind="ACC_OVF", r=0, i=400_000)]
+    # u=3: finite A_r, overflow only after the sum (early decision undecided -> sweep -> skip);
+    # u=4: finite 40000 after the sum (undecided -> sweep -> late apply); u=5, 6: non-finite A_r (early skip)
+    inj = [dict(u=3, kind="RED_OVF", i=262_150), dict(u=4, kind="BIG", i=300_500),
+           dict(u=5, kind="INF", r=world - 1, k=2, i=17), dict(u=6, kind="ACC_OVF", r=0, i=400_000)]
     wl = models.Workload("multi", tensors, world, c, injections=inj, family=family)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)

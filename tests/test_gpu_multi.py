@@ -14,7 +14,7 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-def _run(world, family, updates=6, port=29531):
+def _run(world, family, updates=8, port=29531):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
            str(updates)]

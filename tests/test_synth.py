@@ -74,6 +74,9 @@ def test_injection_overrides():
     assert synth.overrides(wl, 2502, 1, 1) == [(31337, 0)]
     assert synth.overrides(wl, 2503, 2, 16) == [(99991, 0x78E2)]
     assert synth.overrides(wl, 2503, 2, 3) == [(99991, 0)]
+    w2 = models.Workload("b", [("a", 10, 0)], 4, 2, injections=[dict(u=1, kind="BIG", i=3)])
+    assert synth.overrides(w2, 1, 1, 2) == [(3, 0x74E2)] and synth.overrides(w2, 1, 2, 2) == [(3, 0)]
+    assert np.uint16(0x74E2).view(np.float16) == 20000
     with pytest.raises(ValueError):
         synth.overrides(models.Workload("x", [("a", 10, 0)], 1, 2, injections=[dict(u=1, kind="RED_OVF", i=1)]),
                         1, 0, 2)
