@@ -55,6 +55,8 @@ def _load_gpu():
         u64, i64, i32, p = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
         lib.synth_gpu_fill.restype = i32
         lib.synth_gpu_fill.argtypes = [p, i32, p, p, i32, u64, i32, i32, p]
+        lib.synth_gpu_fill_all.restype = i32
+        lib.synth_gpu_fill_all.argtypes = [p, i64, p, p, i32, i32, u64, i32, i32, p]
         lib.synth_gpu_theta0.restype = i32
         lib.synth_gpu_theta0.argtypes = [p, i64, u64, p]
         _glib = lib
@@ -190,9 +192,14 @@ def micro_grad_gpu(out, wl: Workload, lay: Layout, u: int, r: int, k: int, e: in
     import torch
     fam = FAMILIES[family or wl.family]
     s = stream if stream is not None else torch.cuda.current_stream()
-    rc = _load_gpu().synth_gpu_fill(ctypes.c_void_p(out.data_ptr()), lay.n_tensors, _ptr(lay.begin), _ptr(lay.cls),
-                                    fam, key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq),
-                                    ctypes.c_void_p(s.cuda_stream))
+    dev = getattr(lay, "_dev_table", None)
+    if dev is None or dev[0].device != out.device:
+        dev = (torch.from_numpy(lay.begin).to(out.device), torch.from_numpy(lay.cls).to(out.device))
+        lay._dev_table = dev
+    rc = _load_gpu().synth_gpu_fill_all(ctypes.c_void_p(out.data_ptr()), lay.n, ctypes.c_void_p(dev[0].data_ptr()),
+                                        ctypes.c_void_p(dev[1].data_ptr()), lay.n_tensors, fam,
+                                        key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq),
+                                        ctypes.c_void_p(s.cuda_stream))
     if rc != 0:
         raise RuntimeError(f"synth_gpu_fill: cuda error {rc}")
     ov = overrides(wl, u, r, k)
