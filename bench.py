@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--config", default="big_ende", choices=["big_ende", "base", "tiny", "big_enfr"])
     ap.add_argument("--update-freq", type=int, default=None)
     ap.add_argument("--bucket-mib", type=float, default=150.0)
+    ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -212,11 +213,13 @@ def main_ours(args):
         synth.micro_grad_gpu(g, wl, lay, 1, rank, k, 7)
         grads.append(g)
     toks = [synth.ntokens(wl, 1, rank, k) for k in range(1, c + 1)]
-    cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)))
+    cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)),
+                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce])
     # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
     cfg.growth_interval = 1 << 40
     torch.cuda.synchronize()
     step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
+    ar_impl = step.allreduce_impl
     stream = torch.cuda.current_stream()
 
     def one_update():
@@ -353,10 +356,12 @@ def main_ours(args):
         out["exposed_comm"] = {"ms": ms - exposed, "frac_of_update": (ms - exposed) / ms, "t_world1_ms": exposed,
                                "method": "T(update, W ranks) - T(same per-GPU work through a world=1 ctx, same "
                                          "GPU, same run); library-only step (no backward to hide behind)"}
-    if world > 1 and kstat["nccl_allreduce"]["ms"] > 0:
-        ar_ms = kstat["nccl_allreduce"]["ms"] / args.steps
+    if world > 1 and kstat["allreduce"]["ms"] > 0:
+        ar_ms = kstat["allreduce"]["ms"] / args.steps
         bus = 2 * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9
-        out["allreduce"] = {"ms_per_step": ar_ms, "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS}
+        out["allreduce"] = {"impl": {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)), "ms_per_step": ar_ms,
+                            "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS,
+                            "frac_of_770_measured_peer": bus / 770.0}
     if e2e:
         out["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:

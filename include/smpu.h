@@ -63,7 +63,17 @@ typedef struct {
     int64_t growth_interval;   /* 2000 clean updates before the scale doubles                   */
     int32_t update_freq;       /* c >= 1 micro-batches per update ("cumul")                      */
     int64_t bucket_bytes;      /* 150 MiB of fp16 gradient per all-reduce bucket (P:212 footnote, R22)  */
+    int32_t allreduce;         /* world > 1 bucket all-reduce: SMPU_AR_AUTO (fused when every rank is an
+                                  NVLink load/store peer, else NCCL), SMPU_AR_NCCL, SMPU_AR_FUSED          */
 } smpu_config;
+
+/* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */
+enum {
+    SMPU_AR_AUTO = 0,
+    SMPU_AR_NCCL = 1,   /* ncclAllReduce(fp16, sum) per bucket: NCCL's order (R3: not bitwise-pinned for W > 2)  */
+    SMPU_AR_FUSED = 2   /* deterministic reduce-scatter + all-gather kernel over NVLink peer memory (NCCL device
+                           API symmetric window): ascending-rank fp16 sum, bitwise the oracle's for any W      */
+};
 
 typedef struct {
     int32_t overflow;          /* 1 iff the reduced fp16 gradient held a non-finite element     */
@@ -90,7 +100,7 @@ enum {
 
 /* kernel ids of smpu_kernel_stats */
 enum { SMPU_K1_FIRST = 0, SMPU_K1_ADD = 1, SMPU_K1S = 2, SMPU_K0 = 3, SMPU_K2 = 4, SMPU_KCAST = 5,
-       SMPU_NCCL_AR = 6, SMPU_N_KERNELS = 7 };
+       SMPU_ALLREDUCE = 6, SMPU_N_KERNELS = 7 };
 
 int smpu_abi_version(void);
 
@@ -120,6 +130,9 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                       int cuda_device, const int64_t* numel, int n_tensors, const float* init_params);
 
 smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n);
+
+/* Which bucket all-reduce this ctx runs (SMPU_AR_NCCL or SMPU_AR_FUSED; 0 at world == 1). */
+smpu_status smpu_allreduce_impl(const smpu_ctx* ctx, int* impl);
 
 /* Bucket boundaries chosen at init (same as smpu_plan_buckets with cfg->bucket_bytes). */
 smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_begin /* or NULL */);

@@ -1,0 +1,109 @@
+// lsa_allreduce.cuh -- deterministic fused bucket all-reduce over NVLink peer memory.
+//
+// The accumulator is one NCCL symmetric window (ncclMemAlloc + ncclCommWindowRegister), so every rank's
+// accumulator is load/store-accessible from every GPU of the NVLink domain ("LSA" peers, NCCL device API).
+// For bucket [lo, hi) rank r owns shard r (1/W of the bucket).  After a cross-GPU barrier (the last K1 of the
+// bucket has finished on every rank), rank r reads A_0 .. A_{W-1} of its shard from all ranks, sums them in
+// ascending rank order with a round-to-nearest-even fp16 add after each term -- the oracle's order, reading
+// R3, so R is bitwise the oracle's for ANY values, not only exactly-summable ones -- and stores R into the
+// shard of every rank's accumulator (the all-gather).  A second barrier publishes the stores.
+//
+// Bus bytes per rank are those of a ring all-reduce, 2 (W-1)/W x 2 B per element (reads of peer shards in,
+// peer stores out); HBM: the local shard read once, every element of the local accumulator written once.
+#pragma once
+#include <nccl.h>
+#include <nccl_device.h>
+
+#include "kernels.cuh"
+
+namespace smpu {
+
+constexpr int kMaxLsaRanks = 8;
+
+__device__ __forceinline__ V4 ld128_peer(const void* p) {
+    V4 r;
+    asm volatile("ld.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void st128_peer(void* p, const V4& v) {
+    asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
+                 "r"(v.w[3])
+                 : "memory");
+}
+
+// one CTA-wide barrier across the same CTA index of every rank (acquire + release at system scope)
+__device__ __forceinline__ void lsa_sync(const ncclDevComm& dc) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_ar_lsa(ncclDevComm dc, ncclWindow_t win, int64_t lo, int64_t hi) {
+    lsa_sync(dc);   // every rank's last K1 of this bucket is complete and visible
+    uint16_t* base[W];
+#pragma unroll
+    for (int p = 0; p < W; ++p) base[p] = (uint16_t*)ncclGetLsaPointer(win, 0, p);
+    const int me = dc.lsaRank;
+    // shard boundaries on 8-element (16 B) units inside the bucket; shard `me` = [s_lo, s_hi)
+    const int64_t v0 = (lo + 7) & ~(int64_t)7, v1 = hi & ~(int64_t)7;
+    const int64_t units = v1 > v0 ? (v1 - v0) / 8 : 0;
+    const int64_t per = (units + W - 1) / W;
+    int64_t u_lo = me * per, u_hi = u_lo + per;
+    if (u_lo > units) u_lo = units;
+    if (u_hi > units) u_hi = units;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t u = u_lo + tid;
+    for (; u + nthr < u_hi; u += 2 * nthr) {
+        const int64_t i0 = v0 + u * 8, i1 = v0 + (u + nthr) * 8;
+        V4 a[W], b[W];
+#pragma unroll
+        for (int p = 0; p < W; ++p) {
+            a[p] = ld128_peer(base[p] + i0);
+            b[p] = ld128_peer(base[p] + i1);
+        }
+#pragma unroll
+        for (int p = 1; p < W; ++p)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                a[0].w[j] = hadd2_rn(a[0].w[j], a[p].w[j]);
+                b[0].w[j] = hadd2_rn(b[0].w[j], b[p].w[j]);
+            }
+#pragma unroll
+        for (int p = 0; p < W; ++p) {
+            st128_peer(base[p] + i0, a[0]);
+            st128_peer(base[p] + i1, b[0]);
+        }
+    }
+    if (u < u_hi) {
+        const int64_t i0 = v0 + u * 8;
+        V4 a[W];
+#pragma unroll
+        for (int p = 0; p < W; ++p) a[p] = ld128_peer(base[p] + i0);
+#pragma unroll
+        for (int p = 1; p < W; ++p)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[0].w[j] = hadd2_rn(a[0].w[j], a[p].w[j]);
+#pragma unroll
+        for (int p = 0; p < W; ++p) st128_peer(base[p] + i0, a[0]);
+    }
+    // unaligned head [lo, v0) and tail [v1, hi) of the bucket: rank 0 does them element by element
+    if (me == 0) {
+        auto elem = [&](int64_t i) {
+            uint32_t x = base[0][i];
+#pragma unroll
+            for (int p = 1; p < W; ++p) x = hadd2_rn(x, (uint32_t)base[p][i]) & 0xFFFFu;
+#pragma unroll
+            for (int p = 0; p < W; ++p) base[p][i] = (uint16_t)x;
+        };
+        const int64_t head_end = v0 < hi ? v0 : hi;
+        for (int64_t i = lo + tid; i < head_end; i += nthr) elem(i);
+        for (int64_t i = (v1 > head_end ? v1 : head_end) + tid; i < hi; i += nthr) elem(i);
+    }
+    lsa_sync(dc);   // every shard of every rank has been written
+}
+
+}  // namespace smpu

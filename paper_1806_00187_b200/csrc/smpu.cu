@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "lsa_allreduce.cuh"
 #include "smpu.h"
 
 using namespace smpu;
@@ -70,6 +71,12 @@ struct smpu_ctx {
 
     ncclComm_t comm = nullptr;     // gradient buckets
     ncclComm_t comm2 = nullptr;    // the 16-byte decision all-reduce, concurrent with the bucket all-reduces
+    int ar_impl = 0;               // SMPU_AR_NCCL / SMPU_AR_FUSED (world > 1)
+    bool acc_from_nccl = false;    // acc came from ncclMemAlloc (symmetric window)
+    ncclWindow_t win = nullptr;
+    ncclDevComm devcomm{};
+    bool have_devcomm = false;
+    int grid_ar = 0;
     cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
     std::vector<cudaEvent_t> ready, ar_done;
     cudaEvent_t comm_done = nullptr, order_ev = nullptr, dec_ev = nullptr, k2_done = nullptr;
@@ -229,6 +236,22 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
     return SMPU_OK;
 }
 
+smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t cs) {
+    const int g = ctx->grid_ar;
+    switch (ctx->world) {
+        case 2: k_ar_lsa<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        case 3: k_ar_lsa<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        case 4: k_ar_lsa<4><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        case 5: k_ar_lsa<5><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        case 6: k_ar_lsa<6><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        case 7: k_ar_lsa<7><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        case 8: k_ar_lsa<8><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+        default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
+    }
+    CKL("k_ar_lsa");
+    return SMPU_OK;
+}
+
 // issue, in canonical bucket order, the all-reduces of every bucket whose final-micro K1 is enqueued
 smpu_status issue_ready_buckets(smpu_ctx* ctx) {
     while (ctx->next_issue < ctx->nb && ctx->bucket_done[ctx->next_issue]) {
@@ -237,8 +260,14 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
         cudaStream_t cs = ctx->comm_stream;
         CK(cudaStreamWaitEvent(cs, ctx->ready[b], 0));
         {
-            Timed t(ctx, SMPU_NCCL_AR, cs);
-            NK(ncclAllReduce(ctx->acc + lo, ctx->acc + lo, (size_t)(hi - lo), ncclFloat16, ncclSum, ctx->comm, cs));
+            Timed t(ctx, SMPU_ALLREDUCE, cs);
+            if (ctx->ar_impl == SMPU_AR_FUSED) {
+                smpu_status st = launch_ar_fused(ctx, lo, hi, cs);
+                if (st != SMPU_OK) return st;
+            } else {
+                NK(ncclAllReduce(ctx->acc + lo, ctx->acc + lo, (size_t)(hi - lo), ncclFloat16, ncclSum, ctx->comm,
+                                 cs));
+            }
         }
         CK(cudaEventRecord(ctx->ar_done[b], cs));
         ctx->next_issue++;
@@ -313,13 +342,16 @@ void free_ctx(smpu_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->dev);
     cudaDeviceSynchronize();
+    if (c->have_devcomm) ncclDevCommDestroy(c->comm, &c->devcomm);
+    if (c->win) ncclCommWindowDeregister(c->comm, c->win);
     if (c->comm2) ncclCommDestroy(c->comm2);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->theta);
     cudaFree(c->m);
     cudaFree(c->v);
     cudaFree(c->w16);
-    cudaFree(c->acc);
+    if (c->acc_from_nccl) ncclMemFree(c->acc);
+    else cudaFree(c->acc);
     cudaFree(c->flag);
     cudaFree(c->stat);
     cudaFree(c->xs);
@@ -377,6 +409,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->growth_interval = 2000;
     c->update_freq = 1;
     c->bucket_bytes = int64_t(150) << 20;
+    c->allreduce = SMPU_AR_AUTO;
     return SMPU_OK;
 }
 
@@ -449,7 +482,17 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMalloc(&ctx->m, n * 4));
     IK(cudaMalloc(&ctx->v, n * 4));
     IK(cudaMalloc(&ctx->w16, n * 2));
-    IK(cudaMalloc(&ctx->acc, n * 2));
+    const size_t acc_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
+                             NCCL_WIN_REQUIRED_ALIGNMENT;
+    if (world > 1 && cfg->allreduce != SMPU_AR_NCCL && world <= kMaxLsaRanks &&
+        ncclMemAlloc((void**)&ctx->acc, acc_bytes) == ncclSuccess) {
+        ctx->acc_from_nccl = true;
+    } else {
+        if (cfg->allreduce == SMPU_AR_FUSED && world > 1)
+            return bail(set_err(SMPU_EINVAL, "fused all-reduce requested but ncclMemAlloc failed or world > %d",
+                                kMaxLsaRanks));
+        IK(cudaMalloc(&ctx->acc, acc_bytes));
+    }
     IK(cudaMalloc(&ctx->flag, sizeof(int)));
     IK(cudaMalloc(&ctx->stat, sizeof(uint32_t)));
     IK(cudaMalloc(&ctx->xs, 2 * sizeof(int64_t)));
@@ -527,6 +570,24 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclBroadcast", __LINE__));
         r = ncclCommSplit(ctx->comm, 0, rank, &ctx->comm2, nullptr);
         if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclCommSplit", __LINE__));
+        ctx->ar_impl = SMPU_AR_NCCL;
+        if (ctx->acc_from_nccl) {
+            // symmetric window over the accumulator + device communicator with one LSA barrier per CTA
+            ctx->grid_ar = prop.multiProcessorCount * 2;
+            r = ncclCommWindowRegister(ctx->comm, ctx->acc, acc_bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC);
+            if (r == ncclSuccess) {
+                ncclDevCommRequirements reqs;
+                memset(&reqs, 0, sizeof reqs);
+                reqs.lsaBarrierCount = ctx->grid_ar;
+                r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
+                if (r == ncclSuccess) ctx->have_devcomm = true;
+            }
+            if (r == ncclSuccess && ctx->devcomm.lsaSize == world && ctx->devcomm.lsaRank == rank)
+                ctx->ar_impl = SMPU_AR_FUSED;
+            else if (cfg->allreduce == SMPU_AR_FUSED)
+                return bail(set_err(SMPU_EINVAL, "fused all-reduce unavailable (NCCL %d, lsaSize %d of %d)", (int)r,
+                                    ctx->devcomm.lsaSize, world));
+        }
     }
     kc_cast<<<grid_for(n, ctx->grid_k2), 256, 0, s0>>>(ctx->theta, ctx->w16, n);
     ctx->launches[SMPU_KCAST]++;
@@ -540,6 +601,12 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
 smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n) {
     if (!ctx || !n) return set_err(SMPU_EINVAL, "null argument");
     *n = ctx->n;
+    return SMPU_OK;
+}
+
+smpu_status smpu_allreduce_impl(const smpu_ctx* ctx, int* impl) {
+    if (!ctx || !impl) return set_err(SMPU_EINVAL, "null argument");
+    *impl = ctx->world > 1 ? ctx->ar_impl : 0;
     return SMPU_OK;
 }
 

@@ -18,8 +18,9 @@ LIB_PATH = os.path.join(_PKG, "libsmpu.so")
 
 OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EPOISONED = range(7)
 STATE_MASTER, STATE_M, STATE_V, STATE_W16, STATE_ACCUM, STATE_SCALARS = range(6)
-K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, NCCL_AR, N_KERNELS = range(8)
-KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "nccl_allreduce"]
+K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, N_KERNELS = range(8)
+KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "allreduce"]
+AR_AUTO, AR_NCCL, AR_FUSED = range(3)
 NCCL_ID_BYTES = 128
 
 
@@ -34,7 +35,7 @@ class Config(ctypes.Structure):
                 ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("init_scale_log2", ctypes.c_int32),
                 ("min_scale_log2", ctypes.c_int32), ("max_scale_log2", ctypes.c_int32),
                 ("growth_interval", ctypes.c_int64), ("update_freq", ctypes.c_int32),
-                ("bucket_bytes", ctypes.c_int64)]
+                ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32)]
 
 
 class StepResult(ctypes.Structure):
@@ -48,7 +49,7 @@ class StepResult(ctypes.Structure):
 
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
-           "smpu_num_params", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
+           "smpu_num_params", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
            "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_result", "smpu_get_master",
            "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_last_error",
            "smpu_destroy"]
@@ -72,6 +73,7 @@ def lib():
             "smpu_plan_buckets": ([p, i32, i64, P(ctypes.c_int), p], st),
             "smpu_init": ([P(p), P(Config), i32, i32, p, i32, p, i32, p], st),
             "smpu_num_params": ([p, P(ctypes.c_int64)], st),
+            "smpu_allreduce_impl": ([p, P(ctypes.c_int)], st),
             "smpu_buckets": ([p, P(ctypes.c_int), p], st),
             "smpu_weights_fp16": ([p, P(p)], st),
             "smpu_loss_scale": ([p, P(p)], st),
@@ -204,6 +206,12 @@ class UpdateStep:
         return r.as_dict()
 
     # -------------------------------------------------------------- accessors
+    @property
+    def allreduce_impl(self) -> int:
+        v = ctypes.c_int()
+        _check(lib().smpu_allreduce_impl(self._ctx, ctypes.byref(v)))
+        return v.value
+
     @property
     def n_buckets(self):
         return len(self.bucket_begin) - 1

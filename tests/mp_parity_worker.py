@@ -28,6 +28,7 @@ from tests.gpu_util import (RTOL_1, Magnitudes, check_state, decisions, gpu_stat
 def main():
     family = sys.argv[1] if len(sys.argv) > 1 else "exact"
     updates = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    impl = sys.argv[3] if len(sys.argv) > 3 else "auto"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -44,9 +45,14 @@ def main():
     obj = [P.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     # bucket threshold chosen so buckets split the vector at unaligned boundaries
-    step = P.UpdateStep(wl.numel, theta0 if rank == 0 else np.zeros_like(theta0), lib_cfg(wl, bucket_bytes=400_000),
-                        world=world, rank=rank, nccl_id=obj[0], device=local)
+    ar = {"auto": P.smpu.AR_AUTO, "nccl": P.smpu.AR_NCCL, "fused": P.smpu.AR_FUSED}[impl]
+    step = P.UpdateStep(wl.numel, theta0 if rank == 0 else np.zeros_like(theta0),
+                        lib_cfg(wl, bucket_bytes=400_000, allreduce=ar), world=world, rank=rank, nccl_id=obj[0],
+                        device=local)
     assert step.n_buckets >= 2
+    fused = step.allreduce_impl == P.smpu.AR_FUSED
+    if impl == "fused":
+        assert fused
     orc = O.Oracle(theta0) if rank == 0 else None
     mags = Magnitudes(theta0) if rank == 0 else None
     e = 7
@@ -71,7 +77,9 @@ def main():
             ores = orc.update(grads, ntok)
             if ores["applied"]:
                 mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
-            if family == "exact" or world == 2:   # two operands: a + b == b + a, any order is bitwise
+            # bitwise: exactly-summable values (any order), two operands (a + b == b + a), or the fused
+            # all-reduce, which sums in the oracle's ascending rank order
+            if family == "exact" or world == 2 or fused:
                 if decisions(res) != oracle_decisions(ores):
                     failures.append(f"update {u}: decisions {decisions(res)} vs {oracle_decisions(ores)}")
                 nan = np.isnan(ores["R"].view(np.float16))
@@ -101,7 +109,8 @@ def main():
         print("FAIL", *allf, sep="\n")
         sys.exit(1)
     if rank == 0:
-        print(f"multi-GPU parity ok: world={world} family={family} updates={updates}")
+        print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
+              f"(ran {'fused' if fused else 'nccl'})")
 
 
 if __name__ == "__main__":

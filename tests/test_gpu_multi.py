@@ -14,29 +14,39 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-def _run(world, family, updates=8, port=29531):
+def _run(world, family, updates=8, port=29531, impl="auto"):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
-           str(updates)]
+           str(updates), impl]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
 
 
+@pytest.mark.parametrize("impl", ["nccl", "fused"])
 @pytest.mark.parametrize("family", ["exact", "real"])
-def test_world2(family):
+def test_world2(family, impl):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
-    _run(2, family, port=29531 if family == "exact" else 29532)
+    _run(2, family, port=29531 + (family == "real") + 2 * (impl == "fused"), impl=impl)
 
 
-def test_world4_exact():
+@pytest.mark.parametrize("impl", ["nccl", "fused"])
+def test_world4_exact(impl):
     if _ngpu() < 4:
         pytest.skip("needs 4 GPUs")
-    _run(4, "exact", port=29533)
+    _run(4, "exact", port=29541 + (impl == "fused"), impl=impl)
 
 
-def test_world4_real_decisions():
+def test_world4_real_nccl_decisions():
+    """NCCL's fp16 order at W = 4 is not the oracle's (parity unpinned, reading R3): decisions only."""
     if _ngpu() < 4:
         pytest.skip("needs 4 GPUs")
-    _run(4, "real", port=29534)
+    _run(4, "real", port=29543, impl="nccl")
+
+
+def test_world4_real_fused_bitwise():
+    """The fused all-reduce sums in ascending rank order: bitwise the oracle's for G_real at W = 4."""
+    if _ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, "real", port=29544, impl="fused")
