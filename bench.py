@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--update-freq", type=int, default=None)
     ap.add_argument("--bucket-mib", type=float, default=150.0)
     ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
+    ap.add_argument("--mode", choices=["m1", "m2"], default="m1",
+                    help="m1: the update step alone (headline); m2: with a cuBLAS backward-load emulator so the "
+                         "bucket all-reduces overlap backward as in the paper's Fig. 3 (exposed-comm measurement)")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -177,6 +180,129 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------------ M2 backward load
+class BackwardEmulator:
+    """Timing-mode producer: per micro-batch of T target tokens, cuBLAS fp16 GEMMs of every
+    weight matrix's real shape -- forward Y = X W^T, backward dX = dY W and dW = dY^T X (6 n T flops) -- on the
+    library's own fp16 weights (smpu_weights_fp16, "forward-backward computations ... in FP16").
+    Backward runs in gradient-ready order; `on_bucket(b)` fires once the last tensor of bucket b has its
+    dW, which is when the paper adds it to the synchronisation buffer.  Gradient VALUES still come from
+    the synthetic generator: the GEMMs emulate the load the all-reduce must hide behind, nothing more."""
+
+    def __init__(self, wl, w16_ptr, bucket_begin, device, t_max=3500):
+        import torch
+        n = wl.n
+
+        class _View:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f2", "data": (ptr, False),
+                                                 "version": 3}
+        w16 = torch.as_tensor(_View(w16_ptr, n), device=device)
+        d = None
+        for name, numel, _ in wl.tensors:
+            if name.endswith("in_proj.weight"):
+                d = int(round((numel // 3) ** 0.5))
+                break
+        self.mats = []          # (ready index, out, in, view) for every weight matrix
+        off = 0
+        for j, (name, numel, cls) in enumerate(wl.tensors):
+            if name.endswith(".weight") and numel % d == 0 and numel // d > 1 and "ln" not in name.split(".")[-2]:
+                rows = numel // d
+                if name.endswith("fc2.weight"):
+                    shape = (d, numel // d)
+                else:
+                    shape = (rows, d)
+                self.mats.append((j, shape[0], shape[1], w16[off:off + numel].view(shape)))
+            off += numel
+        self.tensor_end = np.cumsum(wl.numel)
+        self.bucket_of_end = {}
+        # bucket b is complete once the tensor ending at bucket_begin[b+1] is done
+        ends = {int(e): j for j, e in enumerate(self.tensor_end)}
+        for b in range(len(bucket_begin) - 1):
+            self.bucket_of_end[ends[int(bucket_begin[b + 1])]] = b
+        dmax = max(max(o, i) for _, o, i, _ in self.mats)
+        self.x = torch.randn(t_max, dmax, device=device, dtype=torch.float16) * 0.1
+        self.dy = torch.randn(t_max, dmax, device=device, dtype=torch.float16) * 0.1
+        self.out = torch.empty(t_max * dmax, device=device, dtype=torch.float16)
+        self.dw = torch.empty(max(o * i for _, o, i, _ in self.mats), device=device, dtype=torch.float16)
+        self.n_tensors = len(wl.tensors)
+        self.flops_per_token = 6 * sum(o * i for _, o, i, _ in self.mats)
+
+    def micro(self, T, on_bucket=None):
+        import torch
+        x, dy = self.x[:T], self.dy[:T]
+        for j, o, i, W in reversed(self.mats):                       # forward: reverse ready order
+            torch.mm(x[:, :i], W.t(), out=self.out[:T * o].view(T, o))
+        by_tensor = {j: (o, i, W) for j, o, i, W in self.mats}
+        for j in range(self.n_tensors):                              # backward: ready order
+            if j in by_tensor:
+                o, i, W = by_tensor[j]
+                torch.mm(dy[:, :o], W, out=self.out[:T * i].view(T, i))                    # dX
+                torch.mm(dy[:, :o].t(), x[:, :i], out=self.dw[:o * i].view(o, i))          # dW
+            if on_bucket is not None and j in self.bucket_of_end:
+                on_bucket(self.bucket_of_end[j])
+
+
+def run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg, theta0):
+    """Whole training-step emulation: c micro-batches of backward load + the update step (library)."""
+    import torch
+    c = wl.update_freq
+
+    def emulator_for(st):
+        return BackwardEmulator(wl, st.weights_fp16_ptr(), st.bucket_begin, f"cuda:{local}")
+
+    def one(st, emu):
+        for k in range(c - 1):
+            emu.micro(toks[k])
+            st.accumulate(grads[k], toks[k], stream)
+        st.micro_begin(toks[c - 1])
+        bb = st.bucket_begin
+        emu.micro(toks[c - 1], on_bucket=lambda b: st.accumulate_bucket(b, grads[c - 1][bb[b]:bb[b + 1]], stream))
+        st.step(stream, wait=False)
+
+    def timed(st, emu, steps):
+        for _ in range(args.warmup):
+            one(st, emu)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            one(st, emu)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return _max_over_ranks(a.elapsed_time(b) / steps, world)
+
+    emu = emulator_for(step)
+    step.kernel_stats(reset=True)
+    step.set_timing(True)
+    ms = timed(step, emu, args.steps)
+    step.set_timing(False)
+    stats = step.kernel_stats(reset=True)
+    # the same per-GPU work with no communication: a world = 1 ctx on the same GPU
+    ms1 = None
+    if world > 1:
+        s1 = P.UpdateStep(wl.numel, theta0, cfg, world=1, rank=0, device=local)
+        ms1 = timed(s1, emulator_for(s1), args.steps)
+        s1.close()
+    if rank != 0:
+        return None
+    out = {"metric": METRIC + " (M2: with emulated backward)", "mode": "m2", "n_gpus": world,
+           "ms_per_step": ms, "steps": args.steps, "warmup": args.warmup,
+           "value": world * c * lay.n / (ms * 1e-3), "unit": UNIT,
+           "config": {"workload": wl.name, "update_freq": c, "bucket_mib": args.bucket_mib,
+                      "allreduce": {0: None, 1: "nccl", 2: "fused_lsa"}[step.allreduce_impl if world > 1 else 0],
+                      "tokens_per_micro": toks, "backward_flops_per_update": emu.flops_per_token * sum(toks)},
+           "update_path_kernels_ms_per_step": stats["k1_add"]["ms"] / args.steps + stats["k1_first"]["ms"] / args.steps
+           + stats["k2_adam"]["ms"] / args.steps,
+           "allreduce_ms_per_step": stats["allreduce"]["ms"] / args.steps}
+    if ms1 is not None:
+        out["exposed_comm"] = {"ms": ms - ms1, "frac_of_update": (ms - ms1) / ms, "t_world1_ms": ms1,
+                               "method": "T(M2 step, W ranks) - T(same per-GPU M2 step through a world=1 ctx)"}
+    return out
+
+
 # ------------------------------------------------------------------------------------------ our arm
 def main_ours(args):
     import torch
@@ -221,6 +347,14 @@ def main_ours(args):
     step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
     ar_impl = step.allreduce_impl
     stream = torch.cuda.current_stream()
+    if args.mode == "m2":
+        out = run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg, theta0)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        step.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     def one_update():
         for k in range(c):
