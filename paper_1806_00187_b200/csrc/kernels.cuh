@@ -168,6 +168,58 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
     if (STATS) publish_max(mx, stat);
 }
 
+// One-shot K1: exactly one 16-half unit per thread, grid = ceil(units / 256), no loop, registers capped for
+// 6+ resident CTAs per SM.  Maximum thread-level parallelism is what saturates HBM on this access mix
+// (tools/hbm_probe.cu: 2R1W one-shot 6.3-6.8 TB/s vs 6.2 for the 4-CTA/SM persistent loop).  The element
+// path (unaligned head / tail / not co-aligned) is taken by the first threads of the grid.
+template <bool FIRST, bool DETECT, bool STATS>
+__global__ void __launch_bounds__(256, 6) k1_accumulate_1(uint16_t* __restrict__ acc, const uint16_t* __restrict__ g,
+                                                          int64_t lo, int64_t hi, int* __restrict__ flag,
+                                                          uint32_t* __restrict__ stat) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const uint16_t* gb = g - lo;
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(gb + vbeg) & 31) == 0);
+    const int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
+    const int64_t vend = vbeg + nvec * 16;
+    uint32_t bad = 0, mx = 0;
+    if (tid < nvec) {
+        const int64_t i0 = vbeg + tid * 16;
+        V8 g0 = ld256_ro(gb + i0);
+        if (!FIRST) {
+            V8 a0 = ld256(acc + i0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g0.w[j] = hadd2_rn(a0.w[j], g0.w[j]);
+        }
+        if (DETECT) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) bad |= nonfinite_bits(g0.w[j]);
+        }
+        if (STATS) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx = mag_max2(mx, g0.w[j]);
+        }
+        st256(acc + i0, g0);
+    }
+    auto elem = [&](int64_t i) {
+        uint16_t x = gb[i];
+        if (!FIRST) x = (uint16_t)(hadd2_rn((uint32_t)acc[i], (uint32_t)x) & 0xFFFFu);
+        if (DETECT && h_nonfinite(x)) bad |= 1u;
+        if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+        acc[i] = x;
+    };
+    if (vec_ok) {
+        for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+        for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
+    }
+    if (DETECT) raise_flag(bad != 0, flag);
+    if (STATS) publish_max(mx, stat);
+}
+
 // ---------------------------------------------------------------------------------------------- K1s
 struct Scalars;
 __device__ __forceinline__ int32_t decision_of(const Scalars* sc);
@@ -415,6 +467,42 @@ __global__ void __launch_bounds__(256) k2_adam(float* __restrict__ theta, float*
     }
     if (u < nvec) {
         const int64_t i0 = vbeg + u * 8;
+        V4 r0 = ld128_ro(R + i0);
+        V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
+        V4 w0;
+        adam_unit(r0, t0, m0, v0, w0, s);
+        st256(theta + i0, t0);
+        st256(m + i0, m0);
+        st256(v + i0, v0);
+        st128(w16 + i0, w0);
+    }
+    auto elem = [&](int64_t i) {
+        float th = theta[i], mm = m[i], vv = v[i];
+        adam_elem(__half2float(__ushort_as_half(R[i])), th, mm, vv, s);
+        theta[i] = th;
+        m[i] = mm;
+        v[i] = vv;
+        w16[i] = __half_as_ushort(__float2half_rn(th));
+    };
+    for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+    for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+}
+
+// One-shot K2: exactly one 8-element unit per thread (112 B in flight), registers capped for 4 resident CTAs
+// per SM; same arithmetic as k2_adam (adam_unit / adam_elem).
+__global__ void __launch_bounds__(256, 4) k2_adam_1(float* __restrict__ theta, float* __restrict__ m,
+                                                    float* __restrict__ v, uint16_t* __restrict__ w16,
+                                                    const uint16_t* __restrict__ R, int64_t lo, int64_t hi,
+                                                    const Scalars* __restrict__ scp, int32_t need) {
+    if (decision_of(scp) != need) return;
+    const Scalars s = *scp;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 7) & ~(int64_t)7;
+    if (vbeg > hi) vbeg = hi;
+    const int64_t nvec = (hi - vbeg) / 8, vend = vbeg + nvec * 8;
+    if (tid < nvec) {
+        const int64_t i0 = vbeg + tid * 8;
         V4 r0 = ld128_ro(R + i0);
         V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
         V4 w0;

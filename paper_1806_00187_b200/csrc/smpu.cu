@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -98,6 +99,7 @@ struct smpu_ctx {
     bool poisoned = false;
 
     int grid_k1 = 0, grid_k2 = 0, grid_k1s = 0;
+    bool k1_oneshot = false, k2_oneshot = false;   // one unit per thread (grid cap "0 CTAs per SM")
 
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -189,6 +191,15 @@ smpu_status leave_stream(smpu_ctx* ctx, cudaStream_t s) {
     return SMPU_OK;
 }
 
+// Grid cap of a streaming kernel: 0 CTAs per SM = one-shot (one unit per thread, no cap; the default for K1
+// and K2, see tools/hbm_probe.cu), else SMs x that many CTAs with a grid-stride loop.  The environment
+// variable `name` overrides the default.
+int grid_cap(const char* name, int sms, int default_cps) {
+    const char* v = getenv(name);
+    int cps = v ? atoi(v) : default_cps;
+    return cps <= 0 ? 0x7fffffff : sms * cps;
+}
+
 int grid_for(int64_t units, int max_grid) {
     int64_t g = (units + 255) / 256;
     if (g > max_grid) g = max_grid;
@@ -201,7 +212,20 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
     if (hi <= lo) return SMPU_OK;
     int grid = grid_for((hi - lo + 15) / 16, ctx->grid_k1);
     Timed t(ctx, first ? SMPU_K1_FIRST : SMPU_K1_ADD, s);
-    if (stats) {
+    if (ctx->k1_oneshot) {
+        uint16_t* a = ctx->acc;
+        int* f = ctx->flag;
+        uint32_t* st = ctx->stat;
+        if (first) {
+            if (stats) k1_accumulate_1<true, false, true><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+            else if (detect) k1_accumulate_1<true, true, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+            else k1_accumulate_1<true, false, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+        } else {
+            if (stats) k1_accumulate_1<false, false, true><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+            else if (detect) k1_accumulate_1<false, true, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+            else k1_accumulate_1<false, false, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+        }
+    } else if (stats) {
         if (first) k1_accumulate<true, false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag, ctx->stat);
         else k1_accumulate<false, false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag, ctx->stat);
     } else if (first) {
@@ -212,6 +236,16 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
         else k1_accumulate<false, false><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag);
     }
     CKL("k1_accumulate");
+    return SMPU_OK;
+}
+
+smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaStream_t s) {
+    int grid = grid_for((hi - lo + 7) / 8, ctx->grid_k2);
+    if (ctx->k2_oneshot)
+        k2_adam_1<<<grid, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, lo, hi, ctx->sc, need);
+    else
+        k2_adam<<<grid, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, lo, hi, ctx->sc, need);
+    CKL("k2_adam");
     return SMPU_OK;
 }
 
@@ -299,9 +333,8 @@ smpu_status issue_decision(smpu_ctx* ctx) {
         int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
         CK(cudaStreamWaitEvent(ks, ctx->ar_done[b], 0));
         Timed t(ctx, SMPU_K2, ks);
-        k2_adam<<<grid_for((hi - lo + 7) / 8, ctx->grid_k2), 256, 0, ks>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
-                                                                           ctx->acc, lo, hi, ctx->sc, DEC_APPLY);
-        CKL("k2_adam");
+        smpu_status st = launch_k2(ctx, lo, hi, DEC_APPLY, ks);
+        if (st != SMPU_OK) return st;
     }
     CK(cudaEventRecord(ctx->k2_done, ks));
     return SMPU_OK;
@@ -529,9 +562,11 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     // persistent grids: resident CTAs per SM x SMs
     int occ = 0;
     IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_accumulate<false, false>, 256, 0));
-    ctx->grid_k1 = prop.multiProcessorCount * (occ > 0 ? occ : 1);
+    ctx->grid_k1 = grid_cap("SMPU_K1_CTAS_PER_SM", prop.multiProcessorCount, 0);
+    ctx->k1_oneshot = ctx->grid_k1 == 0x7fffffff;
     IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_adam, 256, 0));
-    ctx->grid_k2 = prop.multiProcessorCount * (occ > 0 ? occ : 1);
+    ctx->grid_k2 = grid_cap("SMPU_K2_CTAS_PER_SM", prop.multiProcessorCount, 0);
+    ctx->k2_oneshot = ctx->grid_k2 == 0x7fffffff;
     IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1s_sweep, 256, 0));
     ctx->grid_k1s = prop.multiProcessorCount * (occ > 0 ? occ : 1);
 
@@ -744,9 +779,8 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
         }
         {
             Timed t(ctx, SMPU_K2, s);
-            k2_adam<<<ctx->grid_k2, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, 0, ctx->n, ctx->sc,
-                                                 DEC_APPLY_LATE);
-            CKL("k2_adam");
+            smpu_status st2 = launch_k2(ctx, 0, ctx->n, DEC_APPLY_LATE, s);
+            if (st2 != SMPU_OK) return st2;
         }
     } else {
         {
@@ -757,9 +791,8 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
         }
         {
             Timed t(ctx, SMPU_K2, s);
-            k2_adam<<<grid_for((ctx->n + 7) / 8, ctx->grid_k2), 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
-                                                                             ctx->acc, 0, ctx->n, ctx->sc, DEC_APPLY);
-            CKL("k2_adam");
+            smpu_status st2 = launch_k2(ctx, 0, ctx->n, DEC_APPLY, s);
+            if (st2 != SMPU_OK) return st2;
         }
     }
     ctx->attempts++;
