@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--update-freq", type=int, default=None)
     ap.add_argument("--bucket-mib", type=float, default=150.0)
     ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
+    ap.add_argument("--trace", default=None, help="write the timed launches (per stream) as JSONL here")
     ap.add_argument("--mode", choices=["m1", "m2"], default="m1",
                     help="m1: the update step alone (headline); m2: with a cuBLAS backward-load emulator so the "
                          "bucket all-reduces overlap backward as in the paper's Fig. 3 (exposed-comm measurement)")
@@ -389,6 +390,11 @@ def main_ours(args):
         barrier()
     step.set_timing(False)
     ms = ev0.elapsed_time(ev1) / args.steps
+    if args.trace:
+        with open(args.trace if world == 1 else f"{args.trace}.rank{rank}", "w") as f:
+            for kname, sname, a, b in step.kernel_trace():
+                f.write(json.dumps({"rank": rank, "kernel": kname, "stream": sname, "start_ms": round(a, 4),
+                                    "end_ms": round(b, 4)}) + "\n")
     stats = step.kernel_stats(reset=True)
     last = step.result(step.scalars()["attempts"])
     assert last["applied"] == 1 and last["overflow"] == 0, last

@@ -100,7 +100,7 @@ enum {
 
 /* kernel ids of smpu_kernel_stats */
 enum { SMPU_K1_FIRST = 0, SMPU_K1_ADD = 1, SMPU_K1S = 2, SMPU_K0 = 3, SMPU_K2 = 4, SMPU_KCAST = 5,
-       SMPU_ALLREDUCE = 6, SMPU_N_KERNELS = 7 };
+       SMPU_ALLREDUCE = 6, SMPU_DECISION_AR = 7, SMPU_N_KERNELS = 8 };
 
 int smpu_abi_version(void);
 
@@ -185,6 +185,14 @@ smpu_status smpu_set_state(smpu_ctx* ctx, int which, const void* src, int64_t by
 smpu_status smpu_set_timing(smpu_ctx* ctx, int enable);
 smpu_status smpu_kernel_stats(smpu_ctx* ctx, int64_t* launches /* [SMPU_N_KERNELS] */,
                               double* total_ms /* [SMPU_N_KERNELS] or NULL */, int reset);
+
+/* Ordered launch trace of the launches timed since the last smpu_kernel_stats reset (timing enabled): record
+ * i has kernel id kind[i], stream[i] (0 = the caller's, 1 = bucket all-reduce, 2 = decision, 3 = per-bucket
+ * Adam) and start/end in ms relative to the first record (CUDA events on the launching stream).  Arrays hold
+ * `cap` records (any may be NULL); *count receives the total.  Synchronising.  The paper's Fig. 3 (overlap of
+ * backward and synchronisation) is this trace with the producer's own events beside it. */
+smpu_status smpu_kernel_trace(smpu_ctx* ctx, int32_t* kind, int32_t* stream, double* start_ms, double* end_ms,
+                              int64_t cap, int64_t* count);
 
 const char* smpu_last_error(void);
 void smpu_destroy(smpu_ctx* ctx);

@@ -78,6 +78,7 @@ struct smpu_ctx {
     ncclDevComm devcomm{};
     bool have_devcomm = false;
     int grid_ar = 0;
+    size_t dec_area_off = 0;
     cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
     std::vector<cudaEvent_t> ready, ar_done;
     cudaEvent_t comm_done = nullptr, order_ev = nullptr, dec_ev = nullptr, k2_done = nullptr;
@@ -105,6 +106,11 @@ struct smpu_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[SMPU_N_KERNELS];
+    struct TraceRec {
+        int32_t kind, stream;
+        cudaEvent_t b, e;
+    };
+    std::vector<TraceRec> trace;
     int64_t launches[SMPU_N_KERNELS] = {};
 };
 
@@ -174,6 +180,8 @@ struct Timed {
             if (e) {
                 cudaEventRecord(e, s);
                 c->timed[kind].emplace_back(b, e);
+                int sid = s == c->comm_stream ? 1 : s == c->dec_stream ? 2 : s == c->k2_stream ? 3 : 0;
+                c->trace.push_back({kind, sid, b, e});
             }
         }
     }
@@ -241,7 +249,12 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
 
 smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaStream_t s) {
     int grid = grid_for((hi - lo + 7) / 8, ctx->grid_k2);
-    if (ctx->k2_oneshot)
+    if (need == DEC_APPLY_LATE) {
+        // the rare-path fallback: a small persistent grid, so that returning at once (the common case) costs
+        // a few microseconds instead of retiring ~100k one-shot CTAs
+        k2_adam<<<grid_for((hi - lo + 7) / 8, ctx->grid_k1s), 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
+                                                                            ctx->acc, lo, hi, ctx->sc, need);
+    } else if (ctx->k2_oneshot)
         k2_adam_1<<<grid, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, lo, hi, ctx->sc, need);
     else
         k2_adam<<<grid, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, lo, hi, ctx->sc, need);
@@ -313,19 +326,49 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
 // W > 1, once every bucket of the last micro-batch is accumulated: the exact early overflow decision
 // (k0_early) from one 16-byte all-reduce on a second communicator, then Adam per bucket on its own stream,
 // each bucket right behind its gradient all-reduce -- K2 overlaps the remaining all-reduces.
+smpu_status launch_decision_lsa(smpu_ctx* ctx, cudaStream_t ds) {
+    const int par = (int)(ctx->attempts & 1);
+#define SMPU_DEC(WW)                                                                                             \
+    k0_early_lsa<WW><<<1, 32, 0, ds>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, par, ctx->stat,                \
+                                       ctx->local_tokens, ctx->xs, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev,  \
+                                       kRing - 1, ctx->dcfg, (uint32_t)ctx->grid_ar)
+    switch (ctx->world) {
+        case 2: SMPU_DEC(2); break;
+        case 3: SMPU_DEC(3); break;
+        case 4: SMPU_DEC(4); break;
+        case 5: SMPU_DEC(5); break;
+        case 6: SMPU_DEC(6); break;
+        case 7: SMPU_DEC(7); break;
+        case 8: SMPU_DEC(8); break;
+        default: return set_err(SMPU_EINVAL, "fused decision supports 2..8 ranks");
+    }
+#undef SMPU_DEC
+    CKL("k0_early_lsa");
+    return SMPU_OK;
+}
+
 smpu_status issue_decision(smpu_ctx* ctx) {
     cudaStream_t ds = ctx->dec_stream, ks = ctx->k2_stream;
     for (int b = 0; b < ctx->nb; ++b) CK(cudaStreamWaitEvent(ds, ctx->ready[b], 0));
-    {
-        Timed t(ctx, SMPU_K0, ds);
-        k_stats_prep<<<1, 32, 0, ds>>>(ctx->stat, ctx->local_tokens, ctx->xs);
-        CKL("k_stats_prep");
-    }
-    NK(ncclAllReduce(ctx->xs, ctx->xs, 2, ncclInt64, ncclSum, ctx->comm2, ds));   // N and sum_r M_r
-    {
-        Timed t(ctx, SMPU_K0, ds);
-        k0_early<<<1, 32, 0, ds>>>(ctx->xs, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg);
-        CKL("k0_early");
+    if (ctx->ar_impl == SMPU_AR_FUSED) {
+        Timed t(ctx, SMPU_DECISION_AR, ds);
+        smpu_status st = launch_decision_lsa(ctx, ds);
+        if (st != SMPU_OK) return st;
+    } else {
+        {
+            Timed t(ctx, SMPU_K0, ds);
+            k_stats_prep<<<1, 32, 0, ds>>>(ctx->stat, ctx->local_tokens, ctx->xs);
+            CKL("k_stats_prep");
+        }
+        {
+            Timed t(ctx, SMPU_DECISION_AR, ds);
+            NK(ncclAllReduce(ctx->xs, ctx->xs, 2, ncclInt64, ncclSum, ctx->comm2, ds));   // N, sum_r M_r
+        }
+        {
+            Timed t(ctx, SMPU_K0, ds);
+            k0_early<<<1, 32, 0, ds>>>(ctx->xs, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg);
+            CKL("k0_early");
+        }
     }
     CK(cudaEventRecord(ctx->dec_ev, ds));
     CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
@@ -517,8 +560,11 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMalloc(&ctx->w16, n * 2));
     const size_t acc_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
+    // the symmetric window also carries the decision area: 2 parities x world x 16 B
+    const size_t win_bytes = acc_bytes + NCCL_WIN_REQUIRED_ALIGNMENT;
+    ctx->dec_area_off = acc_bytes;
     if (world > 1 && cfg->allreduce != SMPU_AR_NCCL && world <= kMaxLsaRanks &&
-        ncclMemAlloc((void**)&ctx->acc, acc_bytes) == ncclSuccess) {
+        ncclMemAlloc((void**)&ctx->acc, win_bytes) == ncclSuccess) {
         ctx->acc_from_nccl = true;
     } else {
         if (cfg->allreduce == SMPU_AR_FUSED && world > 1)
@@ -609,11 +655,14 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         if (ctx->acc_from_nccl) {
             // symmetric window over the accumulator + device communicator with one LSA barrier per CTA
             ctx->grid_ar = prop.multiProcessorCount * 2;
-            r = ncclCommWindowRegister(ctx->comm, ctx->acc, acc_bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC);
+            r = cudaMemset((char*)ctx->acc + acc_bytes, 0, win_bytes - acc_bytes) == cudaSuccess ? ncclSuccess
+                                                                                              : ncclUnhandledCudaError;
+            if (r == ncclSuccess)
+                r = ncclCommWindowRegister(ctx->comm, ctx->acc, win_bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC);
             if (r == ncclSuccess) {
                 ncclDevCommRequirements reqs;
                 memset(&reqs, 0, sizeof reqs);
-                reqs.lsaBarrierCount = ctx->grid_ar;
+                reqs.lsaBarrierCount = ctx->grid_ar + 1;   // one per all-reduce CTA + the decision exchange
                 r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
                 if (r == ncclSuccess) ctx->have_devcomm = true;
             }
@@ -897,7 +946,30 @@ smpu_status smpu_kernel_stats(smpu_ctx* ctx, int64_t* launches, double* total_ms
             ctx->launches[k] = 0;
             ctx->timed[k].clear();
         }
+        ctx->trace.clear();
         ctx->ev_used = 0;
+    }
+    return SMPU_OK;
+}
+
+smpu_status smpu_kernel_trace(smpu_ctx* ctx, int32_t* kind, int32_t* stream, double* start_ms, double* end_ms,
+                              int64_t cap, int64_t* count) {
+    LIVE(ctx);
+    if (!count || cap < 0) return set_err(SMPU_EINVAL, "null count / negative cap");
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
+    *count = (int64_t)ctx->trace.size();
+    if (ctx->trace.empty()) return SMPU_OK;
+    cudaEvent_t origin = ctx->trace[0].b;
+    for (int64_t i = 0; i < cap && i < (int64_t)ctx->trace.size(); ++i) {
+        const auto& r = ctx->trace[i];
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, origin, r.b));
+        CK(cudaEventElapsedTime(&b, origin, r.e));
+        if (kind) kind[i] = r.kind;
+        if (stream) stream[i] = r.stream;
+        if (start_ms) start_ms[i] = a;
+        if (end_ms) end_ms[i] = b;
     }
     return SMPU_OK;
 }

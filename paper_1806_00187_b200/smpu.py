@@ -18,8 +18,9 @@ LIB_PATH = os.path.join(_PKG, "libsmpu.so")
 
 OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EPOISONED = range(7)
 STATE_MASTER, STATE_M, STATE_V, STATE_W16, STATE_ACCUM, STATE_SCALARS = range(6)
-K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, N_KERNELS = range(8)
-KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "allreduce"]
+K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, DECISION_AR, N_KERNELS = range(9)
+KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "allreduce", "decision_ar"]
+STREAM_NAMES = ["caller", "allreduce", "decision", "adam_per_bucket"]
 AR_AUTO, AR_NCCL, AR_FUSED = range(3)
 NCCL_ID_BYTES = 128
 
@@ -51,7 +52,8 @@ class StepResult(ctypes.Structure):
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
            "smpu_num_params", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
            "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_result", "smpu_get_master",
-           "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_last_error",
+           "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace",
+           "smpu_last_error",
            "smpu_destroy"]
 
 _lib = None
@@ -87,6 +89,7 @@ def lib():
             "smpu_set_state": ([p, i32, p, i64], st),
             "smpu_set_timing": ([p, i32], st),
             "smpu_kernel_stats": ([p, p, p, i32], st),
+            "smpu_kernel_trace": ([p, p, p, p, p, i64, P(ctypes.c_int64)], st),
             "smpu_last_error": ([], ctypes.c_char_p),
             "smpu_destroy": ([p], None),
         }
@@ -260,6 +263,18 @@ class UpdateStep:
         ms = np.zeros(N_KERNELS, dtype=np.float64)
         _check(lib().smpu_kernel_stats(self._ctx, _ptr(launches), _ptr(ms), int(reset)))
         return {KERNEL_NAMES[k]: dict(launches=int(launches[k]), ms=float(ms[k])) for k in range(N_KERNELS)}
+
+    def kernel_trace(self):
+        """[(kernel, stream, start_ms, end_ms)] of the launches timed since the last stats reset."""
+        cnt = ctypes.c_int64()
+        _check(lib().smpu_kernel_trace(self._ctx, None, None, None, None, 0, ctypes.byref(cnt)))
+        m = cnt.value
+        kind = np.zeros(m, np.int32)
+        strm = np.zeros(m, np.int32)
+        t0 = np.zeros(m, np.float64)
+        t1 = np.zeros(m, np.float64)
+        _check(lib().smpu_kernel_trace(self._ctx, _ptr(kind), _ptr(strm), _ptr(t0), _ptr(t1), m, ctypes.byref(cnt)))
+        return [(KERNEL_NAMES[k], STREAM_NAMES[s], a, b) for k, s, a, b in zip(kind, strm, t0, t1)]
 
     def close(self):
         if self._ctx:

@@ -50,3 +50,14 @@ def test_world4_real_fused_bitwise():
     if _ngpu() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, "real", port=29544, impl="fused")
+
+
+def test_c3_enfr_5200_updates_world4():
+    """BASELINE configs[3] at the largest W gpurun grants (4): periodic overflow, skip and regrowth."""
+    if _ngpu() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4", "--master-addr",
+           "127.0.0.1", "--master-port", "29551", "tests/mp_c3_worker.py", "5200"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    print(p.stdout[-3000:], p.stderr[-3000:])
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
