@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--update-freq", type=int, default=None)
     ap.add_argument("--bucket-mib", type=float, default=150.0)
     ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the call-by-call path (c x smpu_accumulate + smpu_step) instead of the captured "
+                         "CUDA graph of the same update (smpu_graph_capture / smpu_graph_launch)")
     ap.add_argument("--trace", default=None, help="write the timed launches (per stream) as JSONL here")
     ap.add_argument("--mode", choices=["m1", "m2"], default="m1",
                     help="m1: the update step alone (headline); m2: with a cuBLAS backward-load emulator so the "
@@ -390,6 +393,7 @@ def main_ours(args):
         barrier()
     step.set_timing(False)
     ms = ev0.elapsed_time(ev1) / args.steps
+    ms_calls = ms
     if args.trace:
         with open(args.trace if world == 1 else f"{args.trace}.rank{rank}", "w") as f:
             for kname, sname, a, b in step.kernel_trace():
@@ -399,12 +403,48 @@ def main_ours(args):
     last = step.result(step.scalars()["attempts"])
     assert last["applied"] == 1 and last["overflow"] == 0, last
 
+    # ---- the same update as one CUDA graph (the headline unless --no-graph): per-kernel event timing cannot see
+    # inside a graph, so the kernel table / roofline above come from the call-by-call region, same kernels
+    graph_info = None
+    if not args.no_graph:
+        step.graph_capture(grads)
+        for _ in range(args.warmup):
+            step.graph_launch(toks, stream)
+        torch.cuda.synchronize()
+        barrier()
+        with Clocks(local) as clk_g:
+            for _ in range(soak):
+                step.graph_launch(toks, stream)
+            step.kernel_stats(reset=True)
+            torch.cuda.synchronize()
+            barrier()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step.graph_launch(toks, stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+        ms = ev0.elapsed_time(ev1) / args.steps
+        gstats = step.kernel_stats(reset=True)
+        last = step.result(step.scalars()["attempts"])
+        assert last["applied"] == 1 and last["overflow"] == 0, last
+        clk = clk_g
+        graph_info = {"ms_per_step_graph": ms, "ms_per_step_calls": ms_calls,
+                      "launches_per_step": sum(v["launches"] for k, v in gstats.items()
+                                               if k not in ("allreduce", "decision_ar")) / args.steps}
+
     # ---- exposed communication: the same per-GPU work through a world = 1 ctx on the same GPU
     exposed = None
     if world > 1:
         step1 = P.UpdateStep(wl.numel, theta0, cfg, world=1, rank=0, device=local)
 
+        if not args.no_graph:
+            step1.graph_capture(grads)
+
         def one_update1():
+            if not args.no_graph:
+                step1.graph_launch(toks, stream)
+                return
             for k in range(c):
                 step1.accumulate(grads[k], toks[k], stream)
             step1.step(stream, wait=False)
@@ -447,6 +487,7 @@ def main_ours(args):
         del host
 
     ms = _max_over_ranks(ms, world)
+    ms_calls = _max_over_ranks(ms_calls, world)
     kstat = {k: {"launches": v["launches"], "ms": _max_over_ranks(v["ms"], world)} for k, v in stats.items()}
     if rank != 0:
         step.close()
@@ -469,7 +510,7 @@ def main_ours(args):
             continue
         bytes_total = bpe * elems_per_step[k] * args.steps
         kernels[k] = {"launches": st["launches"], "avg_us": 1000 * st["ms"] / st["launches"],
-                      "share_of_step": st["ms"] / (ms * args.steps),
+                      "share_of_step": st["ms"] / (ms_calls * args.steps),
                       "algorithmic_bytes_per_launch": bytes_total / st["launches"],
                       "achieved_gbs": bytes_total / (st["ms"] * 1e-3) / 1e9}
     dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
@@ -491,7 +532,11 @@ def main_ours(args):
            "roofline": roof, "kernels": kernels,
            "gpu_launches": int(sum(kstat[k]["launches"] for k in ("k1_first", "k1_add", "k1s_sweep", "k0_decide",
                                                                    "k2_adam"))),
-           "clocks": clk.summary()}
+           "clocks": clk.summary(),
+           "timed_path": "calls (c x smpu_accumulate + smpu_step)" if args.no_graph else
+                         "cuda_graph (smpu_graph_launch of the captured update; kernels/roofline from the call path)"}
+    if graph_info:
+        out["graph"] = {k: (_max_over_ranks(v, 1) if isinstance(v, float) else v) for k, v in graph_info.items()}
     if exposed is not None:
         out["exposed_comm"] = {"ms": ms - exposed, "frac_of_update": (ms - exposed) / ms, "t_world1_ms": exposed,
                                "method": "T(update, W ranks) - T(same per-GPU work through a world=1 ctx, same "

@@ -168,6 +168,18 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* bucket
  * later with smpu_result. */
 smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out);
 
+/* CUDA-graph form of a whole update, for producers with fixed gradient buffers (CUDA graphs instead of a
+ * tracing compiler): smpu_graph_capture records update_freq x smpu_accumulate over micro_grads[0..c) (DEVICE
+ * buffers; their addresses are frozen, their contents are read at replay time) followed by smpu_step into a
+ * graph owned by the ctx (replacing any earlier one).  It enqueues nothing.  At world > 1 it needs the fused
+ * all-reduce (EINVAL with SMPU_AR_NCCL).  smpu_graph_launch replays it on
+ * `stream` with this update's token counts ntokens[0..c) (host): identical arithmetic and decisions to the
+ * call-by-call path, one launch instead of c + 2 (or, at world > 1, the bucket all-reduces, decision and
+ * per-bucket Adam as well); asynchronous, results via smpu_result.  Both ESTATE inside an update.  Launch
+ * counts in smpu_kernel_stats are incremented per replay; per-kernel event timing does not see inside it. */
+smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count);
+smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, void* stream);
+
 /* Result of update attempt `attempt` (1-based; one of the last 64).  Waits for it. */
 smpu_status smpu_result(smpu_ctx* ctx, int64_t attempt, smpu_step_result* out);
 

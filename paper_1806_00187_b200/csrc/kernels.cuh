@@ -355,10 +355,12 @@ __device__ void decide(int overflow, int64_t N, DevState* st, Scalars* sc, float
 }
 
 // W = 1: the last K1 tested the reduced (= local) gradient exactly.
-__global__ void k0_decide(int* __restrict__ flag, int64_t tokens, DevState* __restrict__ st, Scalars* __restrict__ sc,
-                          float* __restrict__ loss_scale, smpu_step_result* __restrict__ ring, int ring_mask,
-                          DevCfg cfg) {
+// tok_ptr != nullptr (CUDA-graph replays): the token count is read from the device at run time
+__global__ void k0_decide(int* __restrict__ flag, int64_t tokens, const int64_t* __restrict__ tok_ptr,
+                          DevState* __restrict__ st, Scalars* __restrict__ sc, float* __restrict__ loss_scale,
+                          smpu_step_result* __restrict__ ring, int ring_mask, DevCfg cfg) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (tok_ptr) tokens = *tok_ptr;
     const int overflow = *(volatile int*)flag != 0;
     *(volatile int*)flag = 0;                          // re-armed for the next update
     decide(overflow, tokens, st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY);
@@ -378,9 +380,10 @@ __device__ __forceinline__ int64_t mag_units(uint32_t bits) {
     return ex == 0 ? (int64_t)man : ((int64_t)(1024 + man)) << (ex - 1);   // |x| / 2^-24
 }
 
-__global__ void k_stats_prep(uint32_t* __restrict__ stat, int64_t local_tokens, int64_t* __restrict__ xs) {
+__global__ void k_stats_prep(uint32_t* __restrict__ stat, int64_t local_tokens, const int64_t* __restrict__ tok_ptr,
+                             int64_t* __restrict__ xs) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    xs[0] = local_tokens;
+    xs[0] = tok_ptr ? *tok_ptr : local_tokens;
     xs[1] = mag_units(*stat);
     *stat = 0;                                         // re-armed for the next update
 }

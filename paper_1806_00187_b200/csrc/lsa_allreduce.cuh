@@ -112,10 +112,13 @@ __global__ void __launch_bounds__(256) k_ar_lsa(ncclDevComm dc, ncclWindow_t win
 // next update cannot overwrite slots not yet read), one LSA barrier, then each rank sums the W slots in rank
 // order -- identical inputs and order on every rank, hence identical decisions -- and decides.
 template <int W>
-__global__ void k0_early_lsa(ncclDevComm dc, ncclWindow_t win, size_t area_off, int parity, uint32_t* stat,
-                             int64_t local_tokens, int64_t* xs, DevState* st, Scalars* sc, float* loss_scale,
-                             smpu_step_result* ring, int ring_mask, DevCfg cfg, uint32_t barrier_index) {
+__global__ void k0_early_lsa(ncclDevComm dc, ncclWindow_t win, size_t area_off, uint32_t* stat,
+                             int64_t local_tokens, const int64_t* tok_ptr, int64_t* xs, DevState* st, Scalars* sc,
+                             float* loss_scale, smpu_step_result* ring, int ring_mask, DevCfg cfg,
+                             uint32_t barrier_index) {
     const int me = dc.lsaRank;
+    if (tok_ptr) local_tokens = *tok_ptr;
+    const int parity = (int)(((volatile const DevState*)st)->attempts & 1);   // same on every rank; graph-safe
     const size_t slot_off = area_off + ((size_t)parity * W + me) * 16;
     if (threadIdx.x == 0) {
         int64_t mine[2] = {local_tokens, mag_units(*stat)};

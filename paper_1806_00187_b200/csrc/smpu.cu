@@ -96,6 +96,12 @@ struct smpu_ctx {
     int buckets_left = 0;
     int next_issue = 0;
     int64_t local_tokens = 0;
+    // CUDA graph of one whole update (smpu_graph_capture / smpu_graph_launch)
+    bool capturing = false;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    int64_t* tok_dev = nullptr;        // this update's local token count, written before each replay
+    int64_t* tok_host = nullptr;       // pinned ring of kRing slots feeding tok_dev
     int64_t attempts = 0;
     bool poisoned = false;
 
@@ -189,10 +195,12 @@ struct Timed {
 
 // order this call's launches after the library's previous writes, whatever stream they were on
 smpu_status enter_stream(smpu_ctx* ctx, cudaStream_t s) {
+    if (ctx->capturing) return SMPU_OK;    // graph launches order themselves (smpu_graph_launch)
     if (ctx->have_order && s != ctx->last_stream) CK(cudaStreamWaitEvent(s, ctx->order_ev, 0));
     return SMPU_OK;
 }
 smpu_status leave_stream(smpu_ctx* ctx, cudaStream_t s) {
+    if (ctx->capturing) return SMPU_OK;
     CK(cudaEventRecord(ctx->order_ev, s));
     ctx->last_stream = s;
     ctx->have_order = true;
@@ -326,12 +334,14 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
 // W > 1, once every bucket of the last micro-batch is accumulated: the exact early overflow decision
 // (k0_early) from one 16-byte all-reduce on a second communicator, then Adam per bucket on its own stream,
 // each bucket right behind its gradient all-reduce -- K2 overlaps the remaining all-reduces.
+// token count source of the decision kernels: kernel argument, or tok_dev inside a captured graph
+const int64_t* tok_src(const smpu_ctx* ctx) { return ctx->capturing ? ctx->tok_dev : nullptr; }
+
 smpu_status launch_decision_lsa(smpu_ctx* ctx, cudaStream_t ds) {
-    const int par = (int)(ctx->attempts & 1);
 #define SMPU_DEC(WW)                                                                                             \
-    k0_early_lsa<WW><<<1, 32, 0, ds>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, par, ctx->stat,                \
-                                       ctx->local_tokens, ctx->xs, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev,  \
-                                       kRing - 1, ctx->dcfg, (uint32_t)ctx->grid_ar)
+    k0_early_lsa<WW><<<1, 32, 0, ds>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->stat,                     \
+                                       ctx->local_tokens, tok_src(ctx), ctx->xs, ctx->st, ctx->sc, ctx->scale,   \
+                                       ctx->ring_dev, kRing - 1, ctx->dcfg, (uint32_t)ctx->grid_ar)
     switch (ctx->world) {
         case 2: SMPU_DEC(2); break;
         case 3: SMPU_DEC(3); break;
@@ -357,7 +367,7 @@ smpu_status issue_decision(smpu_ctx* ctx) {
     } else {
         {
             Timed t(ctx, SMPU_K0, ds);
-            k_stats_prep<<<1, 32, 0, ds>>>(ctx->stat, ctx->local_tokens, ctx->xs);
+            k_stats_prep<<<1, 32, 0, ds>>>(ctx->stat, ctx->local_tokens, tok_src(ctx), ctx->xs);
             CKL("k_stats_prep");
         }
         {
@@ -452,6 +462,10 @@ void free_ctx(smpu_ctx* c) {
     if (c->comm_done) cudaEventDestroy(c->comm_done);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    cudaFree(c->tok_dev);
+    if (c->tok_host) cudaFreeHost(c->tok_host);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
@@ -574,6 +588,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     }
     IK(cudaMalloc(&ctx->flag, sizeof(int)));
     IK(cudaMalloc(&ctx->stat, sizeof(uint32_t)));
+    IK(cudaMalloc(&ctx->tok_dev, sizeof(int64_t)));
+    IK(cudaHostAlloc(&ctx->tok_host, kRing * sizeof(int64_t), cudaHostAllocDefault));
     IK(cudaMalloc(&ctx->xs, 2 * sizeof(int64_t)));
     IK(cudaMalloc(&ctx->st, sizeof(DevState)));
     IK(cudaMalloc(&ctx->sc, sizeof(Scalars)));
@@ -834,8 +850,8 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     } else {
         {
             Timed t(ctx, SMPU_K0, s);
-            k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->local_tokens, ctx->st, ctx->sc, ctx->scale, ctx->ring_dev,
-                                       kRing - 1, ctx->dcfg);
+            k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->local_tokens, tok_src(ctx), ctx->st, ctx->sc, ctx->scale,
+                                       ctx->ring_dev, kRing - 1, ctx->dcfg);
             CKL("k0_decide");
         }
         {
@@ -843,6 +859,13 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
             smpu_status st2 = launch_k2(ctx, 0, ctx->n, DEC_APPLY, s);
             if (st2 != SMPU_OK) return st2;
         }
+    }
+    if (ctx->capturing) {                // smpu_graph_capture restores the host bookkeeping
+        ctx->micro = 0;
+        ctx->local_tokens = 0;
+        ctx->next_issue = 0;
+        std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+        return SMPU_OK;
     }
     ctx->attempts++;
     CK(cudaEventRecord(ctx->ring_ev[(ctx->attempts - 1) % kRing], s));
@@ -857,6 +880,83 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     if (st != SMPU_OK) return st;
     if (out->discarded) return set_err(SMPU_ESTATE, "N = 0 tokens in this update: discarded (reading R19)");
     return SMPU_OK;
+}
+
+smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count) {
+    LIVE(ctx);
+    if (!micro_grads || count != ctx->cfg.update_freq)
+        return set_err(SMPU_EINVAL, "need update_freq = %d micro-gradient buffers", ctx->cfg.update_freq);
+    if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_graph_capture inside an update");
+    if (ctx->world > 1 && ctx->ar_impl != SMPU_AR_FUSED)
+        return set_err(SMPU_EINVAL, "graph capture at world > 1 needs the fused all-reduce (SMPU_AR_FUSED): replays "
+                                    "of captured NCCL collectives on two communicators hung on B200 (2 ranks)");
+    CK(cudaSetDevice(ctx->dev));
+    for (int k = 0; k < count; ++k)
+        if (!micro_grads[k] || classify(micro_grads[k]) != PTR_DEVICE)
+            return set_err(SMPU_EINVAL, "micro_grads[%d] must be a device buffer for graph capture", k);
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    if (ctx->graph_exec) {
+        CK(cudaGraphExecDestroy(ctx->graph_exec));
+        ctx->graph_exec = nullptr;
+    }
+    CK(cudaDeviceSynchronize());
+    const bool timing = ctx->timing;
+    ctx->timing = false;
+    ctx->capturing = true;
+    cudaGraph_t graph = nullptr;
+    smpu_status st = SMPU_OK;
+    cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+        for (int k = 0; k < count && st == SMPU_OK; ++k)
+            st = smpu_accumulate(ctx, micro_grads[k], 0, ctx->cap_stream);
+        if (st == SMPU_OK) st = smpu_step(ctx, ctx->cap_stream, nullptr);
+        cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &graph);
+        if (e == cudaSuccess) e = e2;
+    }
+    ctx->capturing = false;
+    ctx->timing = timing;
+    ctx->micro = 0;
+    ctx->bucket_micro = false;
+    ctx->local_tokens = 0;
+    ctx->next_issue = 0;
+    std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    if (st != SMPU_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (e != cudaSuccess) return fail_cuda(ctx, e, "stream capture of the update", __LINE__);
+    e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail_cuda(ctx, e, "cudaGraphInstantiate", __LINE__);
+    return SMPU_OK;
+}
+
+smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, void* stream) {
+    LIVE(ctx);
+    if (!ctx->graph_exec) return set_err(SMPU_ESTATE, "no captured update graph (smpu_graph_capture)");
+    if (!ntokens || count != ctx->cfg.update_freq) return set_err(SMPU_EINVAL, "need update_freq token counts");
+    if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_graph_launch inside an update");
+    int64_t N = 0;
+    for (int k = 0; k < count; ++k) {
+        if (ntokens[k] < 0) return set_err(SMPU_EINVAL, "ntokens[%d] < 0", k);
+        N += ntokens[k];
+    }
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    smpu_status st = enter_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    const int slot = (int)(ctx->attempts % kRing);
+    if (ctx->attempts >= kRing) CK(cudaEventSynchronize(ctx->ring_ev[slot]));   // slot's previous copy has run
+    ctx->tok_host[slot] = N;
+    CK(cudaMemcpyAsync(ctx->tok_dev, &ctx->tok_host[slot], sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    ctx->launches[SMPU_K1_FIRST] += 1;
+    ctx->launches[SMPU_K1_ADD] += ctx->cfg.update_freq - 1;
+    ctx->launches[SMPU_K0] += 1;
+    ctx->launches[SMPU_K2] += 1;
+    CK(cudaGraphLaunch(ctx->graph_exec, s));
+    ctx->attempts++;
+    CK(cudaEventRecord(ctx->ring_ev[(ctx->attempts - 1) % kRing], s));
+    return leave_stream(ctx, s);
 }
 
 static smpu_status state_array(smpu_ctx* ctx, int which, void** p, int64_t* bytes) {

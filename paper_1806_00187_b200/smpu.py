@@ -51,7 +51,8 @@ class StepResult(ctypes.Structure):
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
            "smpu_num_params", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
-           "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_result", "smpu_get_master",
+           "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_graph_capture", "smpu_graph_launch",
+           "smpu_result", "smpu_get_master",
            "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace",
            "smpu_last_error",
            "smpu_destroy"]
@@ -84,6 +85,8 @@ def lib():
             "smpu_accumulate_bucket": ([p, i32, p, p], st),
             "smpu_step": ([p, p, P(StepResult)], st),
             "smpu_result": ([p, i64, P(StepResult)], st),
+            "smpu_graph_capture": ([p, p, i32], st),
+            "smpu_graph_launch": ([p, p, i32, p], st),
             "smpu_get_master": ([p, p, i64], st),
             "smpu_get_state": ([p, i32, p, i64], st),
             "smpu_set_state": ([p, i32, p, i64], st),
@@ -202,6 +205,15 @@ class UpdateStep:
         r = StepResult()
         _check(lib().smpu_step(self._ctx, _stream(stream), ctypes.byref(r)))
         return r.as_dict()
+
+    def graph_capture(self, micro_grads):
+        """Record update_freq x accumulate(micro_grads[k]) + step as one CUDA graph (device buffers)."""
+        arr = (ctypes.c_void_p * len(micro_grads))(*[_ptr(g).value for g in micro_grads])
+        _check(lib().smpu_graph_capture(self._ctx, arr, len(micro_grads)))
+
+    def graph_launch(self, ntokens, stream=None):
+        toks = np.ascontiguousarray(ntokens, dtype=np.int64)
+        _check(lib().smpu_graph_launch(self._ctx, _ptr(toks), toks.size, _stream(stream)))
 
     def result(self, attempt: int):
         r = StepResult()

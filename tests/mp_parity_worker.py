@@ -29,6 +29,7 @@ def main():
     family = sys.argv[1] if len(sys.argv) > 1 else "exact"
     updates = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     impl = sys.argv[3] if len(sys.argv) > 3 else "auto"
+    use_graph = len(sys.argv) > 4 and sys.argv[4] == "graph"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -57,12 +58,29 @@ def main():
     mags = Magnitudes(theta0) if rank == 0 else None
     e = 7
     failures = []
+    if use_graph:
+        gbufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)]
+        if not fused:      # documented limitation: graphs at W > 1 need the fused all-reduce
+            try:
+                step.graph_capture(gbufs)
+                failures.append("graph capture with the NCCL all-reduce should be refused")
+            except P.SmpuError as ex:
+                assert ex.status == P.smpu.EINVAL
+            use_graph = False
+        else:
+            step.graph_capture(gbufs)
     for u in range(1, updates + 1):
         mine = [synth.micro_grad_cpu(wl, lay, u, rank, k, e) for k in range(1, c + 1)]
         toks = [synth.ntokens(wl, u, rank, k) for k in range(1, c + 1)]
-        for k in range(c):
-            step.accumulate(h2t(mine[k]), toks[k])
-        res = step.step()
+        if use_graph:
+            for k in range(c):
+                gbufs[k].copy_(torch.from_numpy(mine[k].view(np.int16)))
+            step.graph_launch(toks)
+            res = step.result(u)
+        else:
+            for k in range(c):
+                step.accumulate(h2t(mine[k]), toks[k])
+            res = step.step()
         R = step.get_state(P.smpu.STATE_ACCUM)
         st = gpu_state(step)
         h = hashlib.sha256(b"".join(st[x].tobytes() for x in ("theta", "m", "v", "w16"))).hexdigest()
@@ -110,7 +128,7 @@ def main():
         sys.exit(1)
     if rank == 0:
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
-              f"(ran {'fused' if fused else 'nccl'})")
+              f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}")
 
 
 if __name__ == "__main__":

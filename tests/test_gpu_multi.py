@@ -14,10 +14,10 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-def _run(world, family, updates=8, port=29531, impl="auto"):
+def _run(world, family, updates=8, port=29531, impl="auto", graph=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
-           str(updates), impl]
+           str(updates), impl] + (["graph"] if graph else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
@@ -29,6 +29,14 @@ def test_world2(family, impl):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, family, port=29531 + (family == "real") + 2 * (impl == "fused"), impl=impl)
+
+
+@pytest.mark.parametrize("impl", ["nccl", "fused"])
+def test_world2_cuda_graph(impl):
+    """A whole W = 2 update (accumulates, bucket all-reduces, decision exchange, per-bucket Adam) as one graph."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "real", port=29535 + (impl == "fused"), impl=impl, graph=True)
 
 
 @pytest.mark.parametrize("impl", ["nccl", "fused"])

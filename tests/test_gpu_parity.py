@@ -243,3 +243,32 @@ def test_loss_scale_pointer_tracks_scaler(P):
         res = step.step()
         assert scale.item() == 2.0 ** res["scale_log2_next"]
     assert res["overflow"] == 1 and scale.item() == 2.0 ** 6
+
+
+def test_graph_replay_bitwise_equals_call_path(P):
+    """smpu_graph_capture / smpu_graph_launch: the same update as c x accumulate + step, bit for bit, with the
+    token counts read at replay time and the decisions the oracle's (injected overflow at u = 3)."""
+    import torch
+    wl = models.Workload("graph", [("w", 300_001, 0), ("e", 65_536, 2), ("b", 33, 1)], 1, 3,
+                         injections=[dict(u=3, kind="INF", r=0, k=2, i=77)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    b = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    orc = O.Oracle(theta0)
+    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(3)]
+    b.graph_capture(bufs)
+    for u in range(1, 7):
+        e = orc.e
+        grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in (1, 2, 3)]
+        toks = [synth.ntokens(wl, u, 0, k) for k in (1, 2, 3)]
+        ores = orc.update([grads], [toks])
+        for k in range(3):
+            a.accumulate(h2t(grads[k]), toks[k])
+            bufs[k].copy_(torch.from_numpy(grads[k].view(np.int16)))
+        ra = a.step()
+        b.graph_launch(toks)
+        rb = b.result(u)
+        assert decisions(ra) == decisions(rb) == oracle_decisions(ores), u
+        for w in (0, 1, 2, 3, 4, 5):
+            assert np.array_equal(a.get_state(w), b.get_state(w)), (u, w)
