@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--update-freq", type=int, default=None)
     ap.add_argument("--bucket-mib", type=float, default=150.0)
     ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
+    ap.add_argument("--sharded", action="store_true",
+                    help="SURVEY f2 variant: reduce-scatter + Adam on 1/W + all-gather of w16 (not the paper's "
+                         "replicated update; bitwise equal to it, tests/test_gpu_multi.py)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the call-by-call path (c x smpu_accumulate + smpu_step) instead of the captured "
                          "CUDA graph of the same update (smpu_graph_capture / smpu_graph_launch)")
@@ -344,7 +347,8 @@ def main_ours(args):
         grads.append(g)
     toks = [synth.ntokens(wl, 1, rank, k) for k in range(1, c + 1)]
     cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)),
-                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce])
+                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce],
+                           sharded=int(args.sharded and world > 1))
     # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
     cfg.growth_interval = 1 << 40
     torch.cuda.synchronize()
@@ -502,7 +506,8 @@ def main_ours(args):
     # algorithmic bytes per launch: K1 first 4 B/elem, K1 add 6, K1s 2, K2 28
     # (K1s only sweeps when the early decision was undecided; with G_real it returns at once)
     per_elem = {"k1_first": 4, "k1_add": 6, "k2_adam": 28}
-    elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n, "k2_adam": n}
+    elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n,
+                      "k2_adam": sum(h - l for l, h in step.shard_ranges())}
     kernels = {}
     for k, bpe in per_elem.items():
         st = kstat[k]
@@ -525,7 +530,8 @@ def main_ours(args):
            "config": {"workload": wl.name, "n_params": n, "n_tensors": len(wl.numel), "update_freq": c,
                       "world": world, "bucket_mib": args.bucket_mib, "n_buckets": nb,
                       "tokens_per_update": int(sum(toks)) * world, "generator": "G_real (SURVEY 8(d.2))",
-                      "parallelism": f"dp{world}", "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"},
+                      "parallelism": f"dp{world}",
+                      "optimizer": "sharded (SURVEY f2)" if (args.sharded and world > 1) else "replicated (paper)", "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"},
            "update_steps_per_s": 1000.0 / ms,
            "path_hbm_gbs": path_bytes / (ms * 1e-3) / 1e9,
            "path_hbm_frac": path_bytes / (ms * 1e-3) / 1e9 / hbm_peak,

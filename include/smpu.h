@@ -65,6 +65,10 @@ typedef struct {
     int64_t bucket_bytes;      /* 150 MiB of fp16 gradient per all-reduce bucket (P:212 footnote, R22)  */
     int32_t allreduce;         /* world > 1 bucket all-reduce: SMPU_AR_AUTO (fused when every rank is an
                                   NVLink load/store peer, else NCCL), SMPU_AR_NCCL, SMPU_AR_FUSED          */
+    int32_t sharded;           /* 0: the paper's replicated optimizer (every rank updates all of theta).
+                                  1: sharded variant (world > 1, fused all-reduce): reduce-scatter,
+                                  Adam on this rank's shard only, all-gather of w16.  theta/m/v are then valid
+                                  only on smpu_shard_ranges; per element the arithmetic is unchanged.        */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */
@@ -130,6 +134,10 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                       int cuda_device, const int64_t* numel, int n_tensors, const float* init_params);
 
 smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n);
+
+/* Element ranges [ranges[2i], ranges[2i+1]) whose theta/m/v this rank updates (every element when not
+ * sharded).  `ranges` host, capacity 2*cap int64 (NULL to query); *count receives the number of ranges. */
+smpu_status smpu_shard_ranges(const smpu_ctx* ctx, int64_t* ranges, int cap, int* count);
 
 /* Which bucket all-reduce this ctx runs (SMPU_AR_NCCL or SMPU_AR_FUSED; 0 at world == 1). */
 smpu_status smpu_allreduce_impl(const smpu_ctx* ctx, int* impl);

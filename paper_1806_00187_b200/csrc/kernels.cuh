@@ -414,12 +414,15 @@ __global__ void k0_late(int* __restrict__ flag, const int64_t* __restrict__ xs, 
 // Per element (Kingma & Ba Alg. 1 in torch's arrangement, reading R13):
 //   g = fp32(R) * inv_sN;  m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2
 //   theta -= step * m / (sqrt(v) * inv_sqrt_bc2 + eps);  w16 = rn16(theta)
+// Every rounding spelled out with _rn intrinsics: left to the compiler, `a * b + c` is contracted into an FMA
+// differently in the vector and the element paths (seen on hardware as 1-ulp differences of m and v between
+// a bucket's aligned body and its unaligned head), and every path must give the same bits for an element.
 __device__ __forceinline__ void adam_elem(float R, float& th, float& m, float& v, const Scalars& s) {
-    float g = R * s.inv_sN;
-    m = s.b1 * m + s.omb1 * g;
-    v = s.b2 * v + s.omb2 * (g * g);
-    float denom = sqrtf(v) * s.inv_sqrt_bc2 + s.eps;
-    th = th - s.step * (m / denom);
+    const float g = __fmul_rn(R, s.inv_sN);
+    m = __fmaf_rn(s.b1, m, __fmul_rn(s.omb1, g));
+    v = __fmaf_rn(s.b2, v, __fmul_rn(s.omb2, __fmul_rn(g, g)));
+    const float denom = __fmaf_rn(__fsqrt_rn(v), s.inv_sqrt_bc2, s.eps);
+    th = __fmaf_rn(-s.step, __fdiv_rn(m, denom), th);
 }
 
 __device__ __forceinline__ void adam_unit(const V4& r16, V8& th, V8& m, V8& v, V4& w16, const Scalars& s) {

@@ -150,3 +150,135 @@ __global__ void k0_early_lsa(ncclDevComm dc, ncclWindow_t win, size_t area_off, 
 }
 
 }  // namespace smpu
+
+namespace smpu {
+
+// ============================================================================ sharded optimizer
+// An adjacent variant of the paper's replicated update, opt-in (smpu_config.sharded): the bucket all-reduce
+// becomes a reduce-scatter (R of my shard only, same ascending-rank order), Adam runs on my shard only and
+// all-gathers the fp16 weights by storing w16 of the shard into every rank's window.  Per element the
+// arithmetic is exactly the replicated path's, so theta/m/v of a shard and the full w16 are bitwise those of
+// the replicated update; HBM per rank for the optimizer drops from 28 to ~28/W + 2 bytes per element.
+
+// Reduce-scatter of one bucket: like k_ar_lsa, but R is stored into my own window only.  No closing barrier:
+// the end-of-update barrier (k_lsa_barrier) orders every rank's reads of my accumulator before anybody's next
+// update overwrites it.
+template <int W>
+__global__ void __launch_bounds__(256) k_rs_lsa(ncclDevComm dc, ncclWindow_t win, int64_t lo, int64_t hi) {
+    lsa_sync(dc);
+    uint16_t* base[W];
+#pragma unroll
+    for (int p = 0; p < W; ++p) base[p] = (uint16_t*)ncclGetLsaPointer(win, 0, p);
+    const int me = dc.lsaRank;
+    const int64_t v0 = (lo + 7) & ~(int64_t)7, v1 = hi & ~(int64_t)7;
+    const int64_t units = v1 > v0 ? (v1 - v0) / 8 : 0;
+    const int64_t per = (units + W - 1) / W;
+    int64_t u_lo = me * per, u_hi = u_lo + per;
+    if (u_lo > units) u_lo = units;
+    if (u_hi > units) u_hi = units;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = u_lo + tid; u < u_hi; u += nthr) {
+        const int64_t i0 = v0 + u * 8;
+        V4 a[W];
+#pragma unroll
+        for (int p = 0; p < W; ++p) a[p] = ld128_peer(base[p] + i0);
+#pragma unroll
+        for (int p = 1; p < W; ++p)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[0].w[j] = hadd2_rn(a[0].w[j], a[p].w[j]);
+        st128_peer(base[me] + i0, a[0]);
+    }
+    if (me == 0) {
+        auto elem = [&](int64_t i) {
+            uint32_t x = base[0][i];
+#pragma unroll
+            for (int p = 1; p < W; ++p) x = hadd2_rn(x, (uint32_t)base[p][i]) & 0xFFFFu;
+            base[0][i] = (uint16_t)x;
+        };
+        const int64_t head_end = v0 < hi ? v0 : hi;
+        for (int64_t i = lo + tid; i < head_end; i += nthr) elem(i);
+        for (int64_t i = (v1 > head_end ? v1 : head_end) + tid; i < hi; i += nthr) elem(i);
+    }
+}
+
+// Adam on [lo, hi) of my shard (one-shot), w16 stored into every rank's window at window offset w16_off.
+template <int W>
+__global__ void __launch_bounds__(256, 4) k2_adam_shard(ncclWindow_t win, size_t w16_off, float* __restrict__ theta,
+                                                        float* __restrict__ m, float* __restrict__ v,
+                                                        const uint16_t* __restrict__ R, int64_t lo, int64_t hi,
+                                                        const Scalars* __restrict__ scp, int32_t need) {
+    if (decision_of(scp) != need) return;
+    const Scalars s = *scp;
+    uint16_t* wb[W];
+#pragma unroll
+    for (int p = 0; p < W; ++p) wb[p] = (uint16_t*)ncclGetLsaPointer(win, w16_off, p);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 7) & ~(int64_t)7;
+    if (vbeg > hi) vbeg = hi;
+    const int64_t nvec = (hi - vbeg) / 8, vend = vbeg + nvec * 8;
+    for (int64_t u = tid; u < nvec; u += nthr) {
+        const int64_t i0 = vbeg + u * 8;
+        V4 r0 = ld128_ro(R + i0);
+        V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
+        V4 w0;
+        adam_unit(r0, t0, m0, v0, w0, s);
+        st256(theta + i0, t0);
+        st256(m + i0, m0);
+        st256(v + i0, v0);
+#pragma unroll
+        for (int p = 0; p < W; ++p) st128_peer(wb[p] + i0, w0);
+    }
+    auto elem = [&](int64_t i) {
+        float th = theta[i], mm = m[i], vv = v[i];
+        adam_elem(__half2float(__ushort_as_half(R[i])), th, mm, vv, s);
+        theta[i] = th;
+        m[i] = mm;
+        v[i] = vv;
+        uint16_t w = __half_as_ushort(__float2half_rn(th));
+#pragma unroll
+        for (int p = 0; p < W; ++p) wb[p][i] = w;
+    };
+    for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+    for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+}
+
+// One cross-rank barrier (acquire + release, system scope) at barrier index `idx`.
+__global__ void k_lsa_barrier(ncclDevComm dc, uint32_t idx) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), idx);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+// Late decision of the sharded path (only when K0 EARLY was undecided, identically on every rank): each rank
+// swept its own shard of R; the flags are OR-ed through peer memory, then decided as K0 LATE.
+template <int W>
+__global__ void k0_late_lsa(ncclDevComm dc, ncclWindow_t win, size_t area_off, int* flag, const int64_t* xs,
+                            DevState* st, Scalars* sc, float* loss_scale, smpu_step_result* ring, int ring_mask,
+                            DevCfg cfg, uint32_t barrier_index) {
+    if (decision_of(sc) != DEC_UNDECIDED) {
+        if (threadIdx.x == 0) *(volatile int*)flag = 0;
+        return;
+    }
+    const int me = dc.lsaRank;
+    const int parity = (int)(((volatile const DevState*)st)->attempts & 1);
+    area_off += 2 * kMaxLsaRanks * 16;                 // slots of their own: the early exchange may still be read
+    const size_t slot_off = area_off + ((size_t)parity * W + me) * 16;
+    if (threadIdx.x == 0) {
+        const int64_t mine = *(volatile int*)flag != 0;
+        for (int p = 0; p < W; ++p) *(int64_t*)ncclGetLsaPointer(win, slot_off, p) = mine;
+    }
+    {
+        ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), barrier_index);
+        bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    }
+    if (threadIdx.x == 0) {
+        const int64_t* area = (const int64_t*)ncclGetLocalPointer(win, area_off + (size_t)parity * W * 16);
+        int64_t any = 0;
+        for (int p = 0; p < W; ++p) any |= ((volatile const int64_t*)area)[2 * p];
+        decide(any != 0, xs[0], st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY_LATE);
+        *(volatile int*)flag = 0;
+    }
+}
+
+}  // namespace smpu

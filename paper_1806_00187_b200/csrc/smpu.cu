@@ -79,6 +79,9 @@ struct smpu_ctx {
     bool have_devcomm = false;
     int grid_ar = 0;
     size_t dec_area_off = 0;
+    bool sharded = false;                                   // SURVEY f2 variant (smpu_config.sharded)
+    size_t w16_off = 0;                                     // w16 inside the symmetric window
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> shard;   // per bucket: this rank's element ranges
     cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
     std::vector<cudaEvent_t> ready, ar_done;
     cudaEvent_t comm_done = nullptr, order_ev = nullptr, dec_ev = nullptr, k2_done = nullptr;
@@ -255,6 +258,31 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
     return SMPU_OK;
 }
 
+// Adam on this rank's shard ranges of bucket b (sharded variant); one-shot grid, or a small persistent grid for
+// the (normally empty) late fallback
+smpu_status launch_k2_shard(smpu_ctx* ctx, int b, int32_t need, cudaStream_t s) {
+    for (auto& rg : ctx->shard[b]) {
+        if (rg.second <= rg.first) continue;
+        int grid = grid_for((rg.second - rg.first + 7) / 8, need == DEC_APPLY_LATE ? ctx->grid_k1s : 0x7fffffff);
+#define SMPU_K2S(WW)                                                                                            \
+    k2_adam_shard<WW><<<grid, 256, 0, s>>>(ctx->win, ctx->w16_off, ctx->theta, ctx->m, ctx->v, ctx->acc, rg.first, \
+                                           rg.second, ctx->sc, need)
+        switch (ctx->world) {
+            case 2: SMPU_K2S(2); break;
+            case 3: SMPU_K2S(3); break;
+            case 4: SMPU_K2S(4); break;
+            case 5: SMPU_K2S(5); break;
+            case 6: SMPU_K2S(6); break;
+            case 7: SMPU_K2S(7); break;
+            case 8: SMPU_K2S(8); break;
+            default: return set_err(SMPU_EINVAL, "sharded Adam supports 2..8 ranks");
+        }
+#undef SMPU_K2S
+        CKL("k2_adam_shard");
+    }
+    return SMPU_OK;
+}
+
 smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaStream_t s) {
     int grid = grid_for((hi - lo + 7) / 8, ctx->grid_k2);
     if (need == DEC_APPLY_LATE) {
@@ -293,6 +321,20 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
 
 smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t cs) {
     const int g = ctx->grid_ar;
+    if (ctx->sharded) {
+        switch (ctx->world) {
+            case 2: k_rs_lsa<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 3: k_rs_lsa<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 4: k_rs_lsa<4><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 5: k_rs_lsa<5><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 6: k_rs_lsa<6><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 7: k_rs_lsa<7><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 8: k_rs_lsa<8><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            default: return set_err(SMPU_EINVAL, "fused reduce-scatter supports 2..8 ranks");
+        }
+        CKL("k_rs_lsa");
+        return SMPU_OK;
+    }
     switch (ctx->world) {
         case 2: k_ar_lsa<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
         case 3: k_ar_lsa<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
@@ -386,7 +428,7 @@ smpu_status issue_decision(smpu_ctx* ctx) {
         int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
         CK(cudaStreamWaitEvent(ks, ctx->ar_done[b], 0));
         Timed t(ctx, SMPU_K2, ks);
-        smpu_status st = launch_k2(ctx, lo, hi, DEC_APPLY, ks);
+        smpu_status st = ctx->sharded ? launch_k2_shard(ctx, b, DEC_APPLY, ks) : launch_k2(ctx, lo, hi, DEC_APPLY, ks);
         if (st != SMPU_OK) return st;
     }
     CK(cudaEventRecord(ctx->k2_done, ks));
@@ -435,7 +477,7 @@ void free_ctx(smpu_ctx* c) {
     cudaFree(c->theta);
     cudaFree(c->m);
     cudaFree(c->v);
-    cudaFree(c->w16);
+    if (!c->acc_from_nccl) cudaFree(c->w16);
     if (c->acc_from_nccl) ncclMemFree(c->acc);
     else cudaFree(c->acc);
     cudaFree(c->flag);
@@ -500,6 +542,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->update_freq = 1;
     c->bucket_bytes = int64_t(150) << 20;
     c->allreduce = SMPU_AR_AUTO;
+    c->sharded = 0;
     return SMPU_OK;
 }
 
@@ -571,12 +614,18 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMalloc(&ctx->theta, n * 4));
     IK(cudaMalloc(&ctx->m, n * 4));
     IK(cudaMalloc(&ctx->v, n * 4));
-    IK(cudaMalloc(&ctx->w16, n * 2));
+
     const size_t acc_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
     // the symmetric window also carries the decision area: 2 parities x world x 16 B
-    const size_t win_bytes = acc_bytes + NCCL_WIN_REQUIRED_ALIGNMENT;
-    ctx->dec_area_off = acc_bytes;
+    const size_t w16_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
+                             NCCL_WIN_REQUIRED_ALIGNMENT;
+    // window = [acc | w16 | decision area (early + late exchange slots)]
+    const size_t win_bytes = acc_bytes + w16_bytes + NCCL_WIN_REQUIRED_ALIGNMENT;
+    ctx->w16_off = acc_bytes;
+    ctx->dec_area_off = acc_bytes + w16_bytes;
+    if (cfg->sharded && world > 1 && cfg->allreduce == SMPU_AR_NCCL)
+        return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce"));
     if (world > 1 && cfg->allreduce != SMPU_AR_NCCL && world <= kMaxLsaRanks &&
         ncclMemAlloc((void**)&ctx->acc, win_bytes) == ncclSuccess) {
         ctx->acc_from_nccl = true;
@@ -586,6 +635,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                                 kMaxLsaRanks));
         IK(cudaMalloc(&ctx->acc, acc_bytes));
     }
+    if (ctx->acc_from_nccl) ctx->w16 = (uint16_t*)((char*)ctx->acc + ctx->w16_off);
+    else IK(cudaMalloc(&ctx->w16, n * 2));
     IK(cudaMalloc(&ctx->flag, sizeof(int)));
     IK(cudaMalloc(&ctx->stat, sizeof(uint32_t)));
     IK(cudaMalloc(&ctx->tok_dev, sizeof(int64_t)));
@@ -671,14 +722,16 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         if (ctx->acc_from_nccl) {
             // symmetric window over the accumulator + device communicator with one LSA barrier per CTA
             ctx->grid_ar = prop.multiProcessorCount * 2;
-            r = cudaMemset((char*)ctx->acc + acc_bytes, 0, win_bytes - acc_bytes) == cudaSuccess ? ncclSuccess
-                                                                                              : ncclUnhandledCudaError;
+            r = cudaMemset((char*)ctx->acc + ctx->dec_area_off, 0, win_bytes - ctx->dec_area_off) == cudaSuccess
+                    ? ncclSuccess
+                    : ncclUnhandledCudaError;
             if (r == ncclSuccess)
                 r = ncclCommWindowRegister(ctx->comm, ctx->acc, win_bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC);
             if (r == ncclSuccess) {
                 ncclDevCommRequirements reqs;
                 memset(&reqs, 0, sizeof reqs);
-                reqs.lsaBarrierCount = ctx->grid_ar + 1;   // one per all-reduce CTA + the decision exchange
+                // one per all-reduce CTA + early decision + late decision + end-of-update (sharded)
+                reqs.lsaBarrierCount = ctx->grid_ar + 3;
                 r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
                 if (r == ncclSuccess) ctx->have_devcomm = true;
             }
@@ -687,6 +740,29 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
             else if (cfg->allreduce == SMPU_AR_FUSED)
                 return bail(set_err(SMPU_EINVAL, "fused all-reduce unavailable (NCCL %d, lsaSize %d of %d)", (int)r,
                                     ctx->devcomm.lsaSize, world));
+
+            ctx->sharded = cfg->sharded && ctx->ar_impl == SMPU_AR_FUSED;
+            if (ctx->sharded) {
+                // the same shard split as k_rs_lsa: 8-element units, ceil(units / W) per rank, rank 0 also
+                // owns the bucket's unaligned head and tail
+                ctx->shard.resize(ctx->nb);
+                for (int b = 0; b < ctx->nb; ++b) {
+                    const int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
+                    const int64_t v0 = (lo + 7) & ~(int64_t)7, v1 = hi & ~(int64_t)7;
+                    const int64_t units = v1 > v0 ? (v1 - v0) / 8 : 0, per = (units + world - 1) / world;
+                    int64_t u_lo = rank * per, u_hi = u_lo + per;
+                    if (u_lo > units) u_lo = units;
+                    if (u_hi > units) u_hi = units;
+                    ctx->shard[b].push_back({v0 + u_lo * 8, v0 + u_hi * 8});
+                    if (rank == 0) {
+                        const int64_t head_end = v0 < hi ? v0 : hi;
+                        ctx->shard[b].push_back({lo, head_end});
+                        ctx->shard[b].push_back({v1 > head_end ? v1 : head_end, hi});
+                    }
+                }
+            }
+            if (cfg->sharded && !ctx->sharded)
+                return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce (unavailable)"));
         }
     }
     kc_cast<<<grid_for(n, ctx->grid_k2), 256, 0, s0>>>(ctx->theta, ctx->w16, n);
@@ -701,6 +777,30 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
 smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n) {
     if (!ctx || !n) return set_err(SMPU_EINVAL, "null argument");
     *n = ctx->n;
+    return SMPU_OK;
+}
+
+smpu_status smpu_shard_ranges(const smpu_ctx* ctx, int64_t* ranges, int cap, int* count) {
+    if (!ctx || !count) return set_err(SMPU_EINVAL, "null argument");
+    int k = 0;
+    if (!ctx->sharded) {
+        if (ranges && cap > 0) {
+            ranges[0] = 0;
+            ranges[1] = ctx->n;
+        }
+        *count = 1;
+        return SMPU_OK;
+    }
+    for (auto& v : ctx->shard)
+        for (auto& rg : v) {
+            if (rg.second <= rg.first) continue;
+            if (ranges && k < cap) {
+                ranges[2 * k] = rg.first;
+                ranges[2 * k + 1] = rg.second;
+            }
+            ++k;
+        }
+    *count = k;
     return SMPU_OK;
 }
 
@@ -825,7 +925,50 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     cudaStream_t s = (cudaStream_t)stream;
     smpu_status st = enter_stream(ctx, s);
     if (st != SMPU_OK) return st;
-    if (ctx->world > 1) {
+    if (ctx->world > 1 && ctx->sharded) {
+        // sharded variant: sweep my shard of R, OR the flags through peer memory, Adam on my shard (all three
+        // return at once when K0 EARLY decided), then one barrier so that every rank's w16 stores (and reads
+        // of my accumulator) are complete before anybody's next update
+        CK(cudaStreamWaitEvent(s, ctx->comm_done, 0));
+        CK(cudaStreamWaitEvent(s, ctx->k2_done, 0));
+        for (int b = 0; b < ctx->nb; ++b)
+            for (auto& rg : ctx->shard[b]) {
+                if (rg.second <= rg.first) continue;
+                Timed t(ctx, SMPU_K1S, s);
+                k1s_sweep<<<grid_for((rg.second - rg.first + 15) / 16, ctx->grid_k1s), 256, 0, s>>>(
+                    ctx->acc, rg.first, rg.second, ctx->flag, ctx->sc);
+                CKL("k1s_sweep");
+            }
+        {
+            Timed t(ctx, SMPU_K0, s);
+            const uint32_t bi = (uint32_t)ctx->grid_ar + 1;
+#define SMPU_KL(WW)                                                                                           \
+    k0_late_lsa<WW><<<1, 32, 0, s>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->flag, ctx->xs, ctx->st,  \
+                                     ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg, bi)
+            switch (ctx->world) {
+                case 2: SMPU_KL(2); break;
+                case 3: SMPU_KL(3); break;
+                case 4: SMPU_KL(4); break;
+                case 5: SMPU_KL(5); break;
+                case 6: SMPU_KL(6); break;
+                case 7: SMPU_KL(7); break;
+                case 8: SMPU_KL(8); break;
+                default: return set_err(SMPU_EINVAL, "sharded path supports 2..8 ranks");
+            }
+#undef SMPU_KL
+            CKL("k0_late_lsa");
+        }
+        for (int b = 0; b < ctx->nb; ++b) {
+            Timed t(ctx, SMPU_K2, s);
+            smpu_status st2 = launch_k2_shard(ctx, b, DEC_APPLY_LATE, s);
+            if (st2 != SMPU_OK) return st2;
+        }
+        {
+            Timed t(ctx, SMPU_K0, s);
+            k_lsa_barrier<<<1, 32, 0, s>>>(ctx->devcomm, (uint32_t)ctx->grid_ar + 2);
+            CKL("k_lsa_barrier");
+        }
+    } else if (ctx->world > 1) {
         // the exact early decision and the per-bucket Adam are already enqueued (issue_decision); here only
         // the fallback for the rare undecided case: sweep R, decide, Adam on everything.  All three kernels
         // return at once when K0 EARLY decided.

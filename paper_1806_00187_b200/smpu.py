@@ -36,7 +36,7 @@ class Config(ctypes.Structure):
                 ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("init_scale_log2", ctypes.c_int32),
                 ("min_scale_log2", ctypes.c_int32), ("max_scale_log2", ctypes.c_int32),
                 ("growth_interval", ctypes.c_int64), ("update_freq", ctypes.c_int32),
-                ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32)]
+                ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32), ("sharded", ctypes.c_int32)]
 
 
 class StepResult(ctypes.Structure):
@@ -50,7 +50,7 @@ class StepResult(ctypes.Structure):
 
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
-           "smpu_num_params", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
+           "smpu_num_params", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
            "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_graph_capture", "smpu_graph_launch",
            "smpu_result", "smpu_get_master",
            "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace",
@@ -77,6 +77,7 @@ def lib():
             "smpu_init": ([P(p), P(Config), i32, i32, p, i32, p, i32, p], st),
             "smpu_num_params": ([p, P(ctypes.c_int64)], st),
             "smpu_allreduce_impl": ([p, P(ctypes.c_int)], st),
+            "smpu_shard_ranges": ([p, p, i32, P(ctypes.c_int)], st),
             "smpu_buckets": ([p, P(ctypes.c_int), p], st),
             "smpu_weights_fp16": ([p, P(p)], st),
             "smpu_loss_scale": ([p, P(p)], st),
@@ -221,6 +222,14 @@ class UpdateStep:
         return r.as_dict()
 
     # -------------------------------------------------------------- accessors
+    def shard_ranges(self):
+        """[(lo, hi)] element ranges whose theta/m/v this rank updates (everything unless sharded)."""
+        cnt = ctypes.c_int()
+        _check(lib().smpu_shard_ranges(self._ctx, None, 0, ctypes.byref(cnt)))
+        buf = np.zeros(2 * max(cnt.value, 1), dtype=np.int64)
+        _check(lib().smpu_shard_ranges(self._ctx, _ptr(buf), cnt.value, ctypes.byref(cnt)))
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(cnt.value)]
+
     @property
     def allreduce_impl(self) -> int:
         v = ctypes.c_int()

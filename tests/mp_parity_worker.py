@@ -30,6 +30,7 @@ def main():
     updates = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     impl = sys.argv[3] if len(sys.argv) > 3 else "auto"
     use_graph = len(sys.argv) > 4 and sys.argv[4] == "graph"
+    sharded = len(sys.argv) > 4 and sys.argv[4] == "sharded"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -54,6 +55,22 @@ def main():
     fused = step.allreduce_impl == P.smpu.AR_FUSED
     if impl == "fused":
         assert fused
+    shard_step = None
+    if sharded:   # the SURVEY f2 variant beside the replicated ctx, same inputs: must agree bitwise on its shard
+        obj2 = [P.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj2, src=0)
+        shard_step = P.UpdateStep(wl.numel, theta0 if rank == 0 else np.zeros_like(theta0),
+                                  lib_cfg(wl, bucket_bytes=400_000, allreduce=P.smpu.AR_FUSED, sharded=1),
+                                  world=world, rank=rank, nccl_id=obj2[0], device=local)
+        ranges = shard_step.shard_ranges()
+        assert sum(h - l for l, h in ranges) < lay.n
+        cover = [None] * world
+        dist.all_gather_object(cover, ranges)
+        mark = np.zeros(lay.n, np.int32)
+        for rr in cover:
+            for l, h in rr:
+                mark[l:h] += 1
+        assert (mark == 1).all(), "shards must partition the vector"
     orc = O.Oracle(theta0) if rank == 0 else None
     mags = Magnitudes(theta0) if rank == 0 else None
     e = 7
@@ -81,6 +98,21 @@ def main():
             for k in range(c):
                 step.accumulate(h2t(mine[k]), toks[k])
             res = step.step()
+        if shard_step is not None:
+            for k in range(c):
+                shard_step.accumulate(h2t(mine[k]), toks[k])
+            rs = shard_step.step()
+            if decisions(rs) != decisions(res):
+                failures.append(f"update {u}: sharded decisions {decisions(rs)} vs replicated {decisions(res)}")
+            if not np.array_equal(shard_step.get_state(P.smpu.STATE_W16), step.get_state(P.smpu.STATE_W16)):
+                failures.append(f"update {u}: sharded w16 differs from replicated")
+            for which in (P.smpu.STATE_MASTER, P.smpu.STATE_M, P.smpu.STATE_V):
+                a_, b_ = shard_step.get_state(which), step.get_state(which)
+                if not all(np.array_equal(a_[l:h], b_[l:h]) for l, h in ranges):
+                    bad = [(l + int(j), float(a_[l + j]), float(b_[l + j])) for l, h in ranges
+                           for j in np.nonzero(a_[l:h] != b_[l:h])[0][:3]]
+                    failures.append(f"update {u}: sharded state {which} differs on this rank's shard: "
+                                    f"{sum(int((a_[l:h] != b_[l:h]).sum()) for l, h in ranges)} elements, e.g. {bad[:4]}")
         R = step.get_state(P.smpu.STATE_ACCUM)
         st = gpu_state(step)
         h = hashlib.sha256(b"".join(st[x].tobytes() for x in ("theta", "m", "v", "w16"))).hexdigest()
@@ -120,6 +152,8 @@ def main():
         e = res["scale_log2_next"]
     flags = [None] * world
     dist.all_gather_object(flags, failures)
+    if shard_step is not None:
+        shard_step.close()
     step.close()
     dist.destroy_process_group()
     allf = [f for fl in flags for f in fl]
@@ -128,7 +162,8 @@ def main():
         sys.exit(1)
     if rank == 0:
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
-              f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}")
+              f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
+              f"{' + sharded optimizer bitwise' if sharded else ''}")
 
 
 if __name__ == "__main__":

@@ -14,10 +14,10 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-def _run(world, family, updates=8, port=29531, impl="auto", graph=False):
+def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
-           str(updates), impl] + (["graph"] if graph else [])
+           str(updates), impl] + (["graph"] if graph else []) + (["sharded"] if sharded else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
@@ -37,6 +37,15 @@ def test_world2_cuda_graph(impl):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, "real", port=29535 + (impl == "fused"), impl=impl, graph=True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_optimizer_bitwise_equals_replicated(world):
+    """reduce-scatter + Adam on 1/W + all-gather of w16 agrees bit for bit with the paper's replicated
+    update on every rank's shard (theta/m/v) and everywhere (w16), through skips, late decisions and regrowth."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    _run(world, "real", port=29545 + world, impl="fused", sharded=True)
 
 
 @pytest.mark.parametrize("impl", ["nccl", "fused"])
