@@ -436,6 +436,28 @@ def main_ours(args):
         graph_info = {"ms_per_step_graph": ms, "ms_per_step_calls": ms_calls,
                       "launches_per_step": sum(v["launches"] for k, v in gstats.items()
                                                if k not in ("allreduce", "decision_ar")) / args.steps}
+        # variant: the producer keeps all c micro-batch gradients resident (6.7 GB of 180 GB) and the update
+        # accumulates them in one pass (smpu_accumulate_many; bitwise the same sums) -- reported beside the
+        # headline, which keeps the paper's in-place accumulation after every micro-batch
+        step.graph_capture(grads, resident=True)
+        for _ in range(args.warmup):
+            step.graph_launch(toks, stream)
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step.graph_launch(toks, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_res = _max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+        last = step.result(step.scalars()["attempts"])
+        assert last["applied"] == 1 and last["overflow"] == 0, last
+        res_bytes = n * (2 * c + 2 + 28)
+        graph_info["resident_microbatches"] = {
+            "ms_per_step": ms_res, "value": world * c * n / (ms_res * 1e-3), "unit": UNIT,
+            "path_hbm_gbs": res_bytes / (ms_res * 1e-3) / 1e9, "bytes_per_elem": 2 * c + 2 + 28,
+            "api": "smpu_graph_capture(..., SMPU_GRAPH_RESIDENT) -> one smpu_accumulate_many over c buffers"}
 
     # ---- exposed communication: the same per-GPU work through a world = 1 ctx on the same GPU
     exposed = None

@@ -104,7 +104,10 @@ enum {
 
 /* kernel ids of smpu_kernel_stats */
 enum { SMPU_K1_FIRST = 0, SMPU_K1_ADD = 1, SMPU_K1S = 2, SMPU_K0 = 3, SMPU_K2 = 4, SMPU_KCAST = 5,
-       SMPU_ALLREDUCE = 6, SMPU_DECISION_AR = 7, SMPU_N_KERNELS = 8 };
+       SMPU_ALLREDUCE = 6, SMPU_DECISION_AR = 7, SMPU_K1_MANY = 8, SMPU_N_KERNELS = 9 };
+
+/* flags of smpu_graph_capture */
+enum { SMPU_GRAPH_STREAMING = 0, SMPU_GRAPH_RESIDENT = 1 };
 
 int smpu_abi_version(void);
 
@@ -162,6 +165,14 @@ smpu_status smpu_loss_scale(const smpu_ctx* ctx, const float** dev_scale);
  * accumulated.  ESTATE if c micro-batches were already given or a bucket-wise micro-batch is open. */
 smpu_status smpu_accumulate(smpu_ctx* ctx, const void* micro_grads, int64_t ntokens, void* stream);
 
+/* `count` whole micro-batches at once, for producers that keep several micro-batch gradients resident
+ * (B200's 180 GB holds all 16 of Transformer-big, 6.7 GB): equivalent, bit for bit, to `count` consecutive
+ * smpu_accumulate calls (same additions in the same order), in one pass that reads each gradient once
+ * and the accumulator once -- 2 count + 2 (+4) bytes per element instead of 6 count (-2).  micro_grads[k]:
+ * DEVICE fp16[n]; ntokens[k] >= 0; 1 <= count <= 32 and count <= micro-batches left in the update. */
+smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* micro_grads, const int64_t* ntokens, int count,
+                                 void* stream);
+
 /* Bucket-wise micro-batch, for overlap with a still-running backward: micro_begin, then
  * exactly one accumulate_bucket per bucket in any order (buckets are all-reduced in canonical bucket
  * order on every rank).  bucket_grads: host or device fp16 of bucket b only
@@ -179,13 +190,15 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out);
 /* CUDA-graph form of a whole update, for producers with fixed gradient buffers (CUDA graphs instead of a
  * tracing compiler): smpu_graph_capture records update_freq x smpu_accumulate over micro_grads[0..c) (DEVICE
  * buffers; their addresses are frozen, their contents are read at replay time) followed by smpu_step into a
- * graph owned by the ctx (replacing any earlier one).  It enqueues nothing.  At world > 1 it needs the fused
+ * graph owned by the ctx (replacing any earlier one); flags = SMPU_GRAPH_RESIDENT records one
+ * smpu_accumulate_many over all c buffers instead (the producer keeps the c gradients until the replay).
+ * It enqueues nothing.  At world > 1 it needs the fused
  * all-reduce (EINVAL with SMPU_AR_NCCL).  smpu_graph_launch replays it on
  * `stream` with this update's token counts ntokens[0..c) (host): identical arithmetic and decisions to the
  * call-by-call path, one launch instead of c + 2 (or, at world > 1, the bucket all-reduces, decision and
  * per-bucket Adam as well); asynchronous, results via smpu_result.  Both ESTATE inside an update.  Launch
  * counts in smpu_kernel_stats are incremented per replay; per-kernel event timing does not see inside it. */
-smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count);
+smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count, int flags);
 smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, void* stream);
 
 /* Result of update attempt `attempt` (1-based; one of the last 64).  Waits for it. */

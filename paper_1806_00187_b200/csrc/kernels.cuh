@@ -229,6 +229,78 @@ __global__ void __launch_bounds__(256, 6) k1_accumulate_1(uint16_t* __restrict__
     if (STATS) publish_max(mx, stat);
 }
 
+// K1 over several resident micro-batches in one pass (smpu_accumulate_many): per element
+// x = [first ? g_0 : rn16(A + g_0)], then x = rn16(x + g_k) for k = 1..count-1 in order, one store -- the
+// same additions in the same order as `count` K1 launches, bitwise, but each gradient is read once and the
+// accumulator is read/written once: 2 count + 2 (or + 4) bytes per element instead of 6 count (-2).
+constexpr int kMaxMany = 32;
+struct ManyPtrs {
+    const uint16_t* g[kMaxMany];   // g[k][i - lo] is micro-batch k's gradient of element i
+};
+
+template <bool FIRST, bool DETECT, bool STATS>
+__global__ void __launch_bounds__(256, 4) k1_accumulate_many(uint16_t* __restrict__ acc, ManyPtrs P, int count,
+                                                             int64_t lo, int64_t hi, int* __restrict__ flag,
+                                                             uint32_t* __restrict__ stat) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    bool vec_ok = true;
+    for (int k = 0; k < count; ++k) vec_ok &= ((reinterpret_cast<uintptr_t>(P.g[k] + (vbeg - lo)) & 31) == 0);
+    const int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
+    const int64_t vend = vbeg + nvec * 16;
+    uint32_t bad = 0, mx = 0;
+    if (tid < nvec) {
+        const int64_t i0 = vbeg + tid * 16, r0 = i0 - lo;
+        V8 x;
+        int k = 0;
+        if (FIRST) {
+            x = ld256_ro(P.g[0] + r0);
+            k = 1;
+        } else {
+            x = ld256(acc + i0);
+        }
+        // four gradients in flight at a time, added strictly in micro-batch order
+        for (; k < count; k += 4) {
+            V8 y[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < count) y[j] = ld256_ro(P.g[k + j] + r0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < count) {
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) x.w[w] = hadd2_rn(x.w[w], y[j].w[w]);
+                }
+        }
+        if (DETECT) {
+#pragma unroll
+            for (int w = 0; w < 8; ++w) bad |= nonfinite_bits(x.w[w]);
+        }
+        if (STATS) {
+#pragma unroll
+            for (int w = 0; w < 8; ++w) mx = mag_max2(mx, x.w[w]);
+        }
+        st256(acc + i0, x);
+    }
+    auto elem = [&](int64_t i) {
+        uint32_t x = FIRST ? (uint32_t)P.g[0][i - lo] : (uint32_t)acc[i];
+        for (int k = FIRST ? 1 : 0; k < count; ++k) x = hadd2_rn(x, (uint32_t)P.g[k][i - lo]) & 0xFFFFu;
+        if (DETECT && h_nonfinite((uint16_t)x)) bad |= 1u;
+        if (STATS) mx = max(mx, x & 0x7FFFu);
+        acc[i] = (uint16_t)x;
+    };
+    if (vec_ok) {
+        for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+        for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
+    }
+    if (DETECT) raise_flag(bad != 0, flag);
+    if (STATS) publish_max(mx, stat);
+}
+
 // ---------------------------------------------------------------------------------------------- K1s
 struct Scalars;
 __device__ __forceinline__ int32_t decision_of(const Scalars* sc);

@@ -103,6 +103,7 @@ struct smpu_ctx {
     bool capturing = false;
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    bool graph_resident = false;
     int64_t* tok_dev = nullptr;        // this update's local token count, written before each replay
     int64_t* tok_host = nullptr;       // pinned ring of kRing slots feeding tok_dev
     int64_t attempts = 0;
@@ -346,6 +347,29 @@ smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
         default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
     }
     CKL("k_ar_lsa");
+    return SMPU_OK;
+}
+
+smpu_status launch_k1_many(smpu_ctx* ctx, const uint16_t* const* g, int count, int64_t lo, int64_t hi, bool first,
+                           bool detect, bool stats, cudaStream_t s) {
+    if (hi <= lo) return SMPU_OK;
+    ManyPtrs P;
+    for (int k = 0; k < count; ++k) P.g[k] = g[k] + lo;
+    int grid = grid_for((hi - lo + 15) / 16, 0x7fffffff);
+    Timed t(ctx, SMPU_K1_MANY, s);
+    uint16_t* a = ctx->acc;
+    int* f = ctx->flag;
+    uint32_t* st = ctx->stat;
+    if (first) {
+        if (stats) k1_accumulate_many<true, false, true><<<grid, 256, 0, s>>>(a, P, count, lo, hi, f, st);
+        else if (detect) k1_accumulate_many<true, true, false><<<grid, 256, 0, s>>>(a, P, count, lo, hi, f, st);
+        else k1_accumulate_many<true, false, false><<<grid, 256, 0, s>>>(a, P, count, lo, hi, f, st);
+    } else {
+        if (stats) k1_accumulate_many<false, false, true><<<grid, 256, 0, s>>>(a, P, count, lo, hi, f, st);
+        else if (detect) k1_accumulate_many<false, true, false><<<grid, 256, 0, s>>>(a, P, count, lo, hi, f, st);
+        else k1_accumulate_many<false, false, false><<<grid, 256, 0, s>>>(a, P, count, lo, hi, f, st);
+    }
+    CKL("k1_accumulate_many");
     return SMPU_OK;
 }
 
@@ -904,6 +928,47 @@ smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, v
     return leave_stream(ctx, s);
 }
 
+smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const int64_t* ntokens, int count,
+                                 void* stream) {
+    LIVE(ctx);
+    if (!grads || !ntokens || count < 1 || count > kMaxMany) return set_err(SMPU_EINVAL, "need 1..%d buffers", kMaxMany);
+    if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "a bucket-wise micro-batch is open");
+    if (ctx->micro + count > ctx->cfg.update_freq)
+        return set_err(SMPU_ESTATE, "%d + %d micro-batches exceed update_freq %d", ctx->micro, count,
+                       ctx->cfg.update_freq);
+    CK(cudaSetDevice(ctx->dev));
+    const uint16_t* g[kMaxMany];
+    for (int k = 0; k < count; ++k) {
+        if (ntokens[k] < 0) return set_err(SMPU_EINVAL, "ntokens[%d] < 0", k);
+        if (!grads[k] || classify(grads[k]) != PTR_DEVICE)
+            return set_err(SMPU_EINVAL, "micro_grads[%d] must be a device buffer", k);
+        g[k] = (const uint16_t*)grads[k];
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    smpu_status st = enter_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    const bool first = ctx->micro == 0;
+    for (int k = 0; k < count; ++k) start_micro(ctx, ntokens[k]);
+    const bool last = final_micro(ctx);
+    if (last && ctx->world > 1) {
+        // bucket by bucket, so that bucket b's all-reduce overlaps the accumulation of buckets > b
+        for (int b = 0; b < ctx->nb; ++b) {
+            st = launch_k1_many(ctx, g, count, ctx->bbegin[b], ctx->bbegin[b + 1], first, false, true, s);
+            if (st != SMPU_OK) return st;
+            ctx->bucket_done[b] = 1;
+            CK(cudaEventRecord(ctx->ready[b], s));
+            st = issue_ready_buckets(ctx);
+            if (st != SMPU_OK) return st;
+        }
+        st = leave_stream(ctx, s);
+        if (st != SMPU_OK) return st;
+        return issue_decision(ctx);
+    }
+    st = launch_k1_many(ctx, g, count, 0, ctx->n, first, last, false, s);
+    if (st != SMPU_OK) return st;
+    return leave_stream(ctx, s);
+}
+
 smpu_status smpu_result(smpu_ctx* ctx, int64_t attempt, smpu_step_result* out) {
     LIVE(ctx);
     if (!out) return set_err(SMPU_EINVAL, "null out");
@@ -1025,7 +1090,7 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     return SMPU_OK;
 }
 
-smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count) {
+smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count, int flags) {
     LIVE(ctx);
     if (!micro_grads || count != ctx->cfg.update_freq)
         return set_err(SMPU_EINVAL, "need update_freq = %d micro-gradient buffers", ctx->cfg.update_freq);
@@ -1050,8 +1115,13 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     smpu_status st = SMPU_OK;
     cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
     if (e == cudaSuccess) {
-        for (int k = 0; k < count && st == SMPU_OK; ++k)
-            st = smpu_accumulate(ctx, micro_grads[k], 0, ctx->cap_stream);
+        if (flags & SMPU_GRAPH_RESIDENT) {
+            std::vector<int64_t> zeros(count, 0);
+            st = smpu_accumulate_many(ctx, micro_grads, zeros.data(), count, ctx->cap_stream);
+        } else {
+            for (int k = 0; k < count && st == SMPU_OK; ++k)
+                st = smpu_accumulate(ctx, micro_grads[k], 0, ctx->cap_stream);
+        }
         if (st == SMPU_OK) st = smpu_step(ctx, ctx->cap_stream, nullptr);
         cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &graph);
         if (e == cudaSuccess) e = e2;
@@ -1068,6 +1138,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
         return st;
     }
     if (e != cudaSuccess) return fail_cuda(ctx, e, "stream capture of the update", __LINE__);
+    ctx->graph_resident = (flags & SMPU_GRAPH_RESIDENT) != 0;
     e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail_cuda(ctx, e, "cudaGraphInstantiate", __LINE__);
@@ -1092,8 +1163,12 @@ smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, 
     if (ctx->attempts >= kRing) CK(cudaEventSynchronize(ctx->ring_ev[slot]));   // slot's previous copy has run
     ctx->tok_host[slot] = N;
     CK(cudaMemcpyAsync(ctx->tok_dev, &ctx->tok_host[slot], sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    ctx->launches[SMPU_K1_FIRST] += 1;
-    ctx->launches[SMPU_K1_ADD] += ctx->cfg.update_freq - 1;
+    if (ctx->graph_resident) {
+        ctx->launches[SMPU_K1_MANY] += ctx->world > 1 ? ctx->nb : 1;
+    } else {
+        ctx->launches[SMPU_K1_FIRST] += 1;
+        ctx->launches[SMPU_K1_ADD] += ctx->cfg.update_freq - 1;
+    }
     ctx->launches[SMPU_K0] += 1;
     ctx->launches[SMPU_K2] += 1;
     CK(cudaGraphLaunch(ctx->graph_exec, s));

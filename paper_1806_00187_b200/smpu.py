@@ -18,8 +18,10 @@ LIB_PATH = os.path.join(_PKG, "libsmpu.so")
 
 OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EPOISONED = range(7)
 STATE_MASTER, STATE_M, STATE_V, STATE_W16, STATE_ACCUM, STATE_SCALARS = range(6)
-K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, DECISION_AR, N_KERNELS = range(9)
-KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "allreduce", "decision_ar"]
+K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, DECISION_AR, K1_MANY, N_KERNELS = range(10)
+KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "allreduce", "decision_ar",
+                "k1_many"]
+GRAPH_STREAMING, GRAPH_RESIDENT = 0, 1
 STREAM_NAMES = ["caller", "allreduce", "decision", "adam_per_bucket"]
 AR_AUTO, AR_NCCL, AR_FUSED = range(3)
 NCCL_ID_BYTES = 128
@@ -51,7 +53,7 @@ class StepResult(ctypes.Structure):
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
            "smpu_num_params", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
-           "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_graph_capture", "smpu_graph_launch",
+           "smpu_accumulate_many", "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_graph_capture", "smpu_graph_launch",
            "smpu_result", "smpu_get_master",
            "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace",
            "smpu_last_error",
@@ -83,10 +85,11 @@ def lib():
             "smpu_loss_scale": ([p, P(p)], st),
             "smpu_accumulate": ([p, p, i64, p], st),
             "smpu_micro_begin": ([p, i64], st),
+            "smpu_accumulate_many": ([p, p, p, i32, p], st),
             "smpu_accumulate_bucket": ([p, i32, p, p], st),
             "smpu_step": ([p, p, P(StepResult)], st),
             "smpu_result": ([p, i64, P(StepResult)], st),
-            "smpu_graph_capture": ([p, p, i32], st),
+            "smpu_graph_capture": ([p, p, i32, i32], st),
             "smpu_graph_launch": ([p, p, i32, p], st),
             "smpu_get_master": ([p, p, i64], st),
             "smpu_get_state": ([p, i32, p, i64], st),
@@ -207,10 +210,16 @@ class UpdateStep:
         _check(lib().smpu_step(self._ctx, _stream(stream), ctypes.byref(r)))
         return r.as_dict()
 
-    def graph_capture(self, micro_grads):
-        """Record update_freq x accumulate(micro_grads[k]) + step as one CUDA graph (device buffers)."""
+    def accumulate_many(self, micro_grads, ntokens, stream=None):
         arr = (ctypes.c_void_p * len(micro_grads))(*[_ptr(g).value for g in micro_grads])
-        _check(lib().smpu_graph_capture(self._ctx, arr, len(micro_grads)))
+        toks = np.ascontiguousarray(ntokens, dtype=np.int64)
+        _check(lib().smpu_accumulate_many(self._ctx, arr, _ptr(toks), len(micro_grads), _stream(stream)))
+
+    def graph_capture(self, micro_grads, resident: bool = False):
+        """Record update_freq x accumulate(micro_grads[k]) + step as one CUDA graph (device buffers);
+        resident=True records one accumulate_many over all of them instead."""
+        arr = (ctypes.c_void_p * len(micro_grads))(*[_ptr(g).value for g in micro_grads])
+        _check(lib().smpu_graph_capture(self._ctx, arr, len(micro_grads), GRAPH_RESIDENT if resident else 0))
 
     def graph_launch(self, ntokens, stream=None):
         toks = np.ascontiguousarray(ntokens, dtype=np.int64)

@@ -31,6 +31,7 @@ def main():
     impl = sys.argv[3] if len(sys.argv) > 3 else "auto"
     use_graph = len(sys.argv) > 4 and sys.argv[4] == "graph"
     sharded = len(sys.argv) > 4 and sys.argv[4] == "sharded"
+    many = len(sys.argv) > 4 and sys.argv[4] == "many"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -94,6 +95,10 @@ def main():
                 gbufs[k].copy_(torch.from_numpy(mine[k].view(np.int16)))
             step.graph_launch(toks)
             res = step.result(u)
+        elif many:     # resident micro-batches: the first one alone, then the rest (incl. the final) in one pass
+            step.accumulate(h2t(mine[0]), toks[0])
+            step.accumulate_many([h2t(x) for x in mine[1:]], toks[1:])
+            res = step.step()
         else:
             for k in range(c):
                 step.accumulate(h2t(mine[k]), toks[k])
@@ -163,7 +168,7 @@ def main():
     if rank == 0:
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
               f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
-              f"{' + sharded optimizer bitwise' if sharded else ''}")
+              f"{' + sharded optimizer bitwise' if sharded else ''}{' via accumulate_many' if many else ''}")
 
 
 if __name__ == "__main__":

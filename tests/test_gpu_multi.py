@@ -14,10 +14,11 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False):
+def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False, many=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
-           str(updates), impl] + (["graph"] if graph else []) + (["sharded"] if sharded else [])
+           str(updates), impl] + (["graph"] if graph else []) + (["sharded"] if sharded else []) + \
+          (["many"] if many else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
@@ -37,6 +38,13 @@ def test_world2_cuda_graph(impl):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, "real", port=29535 + (impl == "fused"), impl=impl, graph=True)
+
+
+def test_world2_accumulate_many_final_microbatch():
+    """smpu_accumulate_many covering the final micro-batch at W = 2 (per-bucket passes + all-reduces)."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "real", port=29539, impl="fused", many=True)
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -272,3 +272,43 @@ def test_graph_replay_bitwise_equals_call_path(P):
         assert decisions(ra) == decisions(rb) == oracle_decisions(ores), u
         for w in (0, 1, 2, 3, 4, 5):
             assert np.array_equal(a.get_state(w), b.get_state(w)), (u, w)
+
+
+def test_accumulate_many_bitwise_equals_streaming(P):
+    """smpu_accumulate_many (resident micro-batches, one pass) == consecutive smpu_accumulate calls, bit for bit,
+    on ragged tensors, mixed with single calls, and as a resident CUDA graph; decisions are the oracle's."""
+    import torch
+    tensors = [("a", 17, 1), ("b", 100_003, 0), ("c", 65_536, 2), ("d", 5, 1), ("e", 250_001, 0)]
+    wl = models.Workload("many", tensors, 1, 5, injections=[dict(u=2, kind="NAN", r=0, k=4, i=100_010),
+                                                            dict(u=4, kind="ACC_OVF", r=0, i=77)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    b = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    g = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    orc = O.Oracle(theta0)
+    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(5)]
+    g.graph_capture(bufs, resident=True)
+    for u in range(1, 6):
+        e = orc.e
+        grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in range(1, 6)]
+        toks = [synth.ntokens(wl, u, 0, k) for k in range(1, 6)]
+        ores = orc.update([grads], [toks])
+        dev = [h2t(x) for x in grads]
+        for k in range(5):
+            a.accumulate(dev[k], toks[k])
+            bufs[k].copy_(dev[k])
+        ra = a.step()
+        b.accumulate_many(dev[:2], toks[:2])          # groups of 2, 1, 2
+        b.accumulate(dev[2], toks[2])
+        b.accumulate_many(dev[3:], toks[3:])
+        rb = b.step()
+        g.graph_launch(toks)
+        rg = g.result(u)
+        assert decisions(ra) == decisions(rb) == decisions(rg) == oracle_decisions(ores), u
+        for w in (0, 1, 2, 3, 4, 5):
+            sa = a.get_state(w)
+            assert np.array_equal(sa, b.get_state(w)) and np.array_equal(sa, g.get_state(w)), (u, w)
+    with pytest.raises(P.SmpuError) as ei:
+        b.accumulate_many(dev + [dev[0]], toks + [1])     # 6 micro-batches with update_freq 5
+    assert ei.value.status == P.smpu.ESTATE
