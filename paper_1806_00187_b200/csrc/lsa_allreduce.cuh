@@ -34,6 +34,21 @@ __device__ __forceinline__ void st128_peer(void* p, const V4& v) {
                  : "memory");
 }
 
+__device__ __forceinline__ V8 ld256_peer(const void* p) {
+    V8 r;
+    asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                   "=r"(r.w[6]), "=r"(r.w[7])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void st256_peer(void* p, const V8& v) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
+                 "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+
 // one CTA-wide barrier across the same CTA index of every rank (acquire + release at system scope)
 __device__ __forceinline__ void lsa_sync(const ncclDevComm& dc) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
@@ -104,6 +119,50 @@ __global__ void __launch_bounds__(256) k_ar_lsa(ncclDevComm dc, ncclWindow_t win
         for (int64_t i = (v1 > head_end ? v1 : head_end) + tid; i < hi; i += nthr) elem(i);
     }
     lsa_sync(dc);   // every shard of every rank has been written
+}
+
+// Variant with 32-byte units (256-bit peer loads/stores), one unit per thread per iteration: fewer, wider NVLink
+// transactions.  Shards are split on 16-element units; head/tail on rank 0 as above.
+template <int W>
+__global__ void __launch_bounds__(256) k_ar_lsa32(ncclDevComm dc, ncclWindow_t win, int64_t lo, int64_t hi) {
+    lsa_sync(dc);
+    uint16_t* base[W];
+#pragma unroll
+    for (int p = 0; p < W; ++p) base[p] = (uint16_t*)ncclGetLsaPointer(win, 0, p);
+    const int me = dc.lsaRank;
+    const int64_t v0 = (lo + 15) & ~(int64_t)15, v1 = hi & ~(int64_t)15;
+    const int64_t units = v1 > v0 ? (v1 - v0) / 16 : 0;
+    const int64_t per = (units + W - 1) / W;
+    int64_t u_lo = me * per, u_hi = u_lo + per;
+    if (u_lo > units) u_lo = units;
+    if (u_hi > units) u_hi = units;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = u_lo + tid; u < u_hi; u += nthr) {
+        const int64_t i0 = v0 + u * 16;
+        V8 a[W];
+#pragma unroll
+        for (int p = 0; p < W; ++p) a[p] = ld256_peer(base[p] + i0);
+#pragma unroll
+        for (int p = 1; p < W; ++p)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[0].w[j] = hadd2_rn(a[0].w[j], a[p].w[j]);
+#pragma unroll
+        for (int p = 0; p < W; ++p) st256_peer(base[p] + i0, a[0]);
+    }
+    if (me == 0) {
+        auto elem = [&](int64_t i) {
+            uint32_t x = base[0][i];
+#pragma unroll
+            for (int p = 1; p < W; ++p) x = hadd2_rn(x, (uint32_t)base[p][i]) & 0xFFFFu;
+#pragma unroll
+            for (int p = 0; p < W; ++p) base[p][i] = (uint16_t)x;
+        };
+        const int64_t head_end = v0 < hi ? v0 : hi;
+        for (int64_t i = lo + tid; i < head_end; i += nthr) elem(i);
+        for (int64_t i = (v1 > head_end ? v1 : head_end) + tid; i < hi; i += nthr) elem(i);
+    }
+    lsa_sync(dc);
 }
 
 // The early overflow decision of K0 EARLY with the 16-byte exchange done in peer memory instead of an NCCL

@@ -78,6 +78,7 @@ struct smpu_ctx {
     ncclDevComm devcomm{};
     bool have_devcomm = false;
     int grid_ar = 0;
+    bool ar_vec32 = false;                                  // 256-bit peer accesses in the fused all-reduce
     size_t dec_area_off = 0;
     bool sharded = false;                                   // SURVEY f2 variant (smpu_config.sharded)
     size_t w16_off = 0;                                     // w16 inside the symmetric window
@@ -334,6 +335,20 @@ smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
             default: return set_err(SMPU_EINVAL, "fused reduce-scatter supports 2..8 ranks");
         }
         CKL("k_rs_lsa");
+        return SMPU_OK;
+    }
+    if (ctx->ar_vec32) {
+        switch (ctx->world) {
+            case 2: k_ar_lsa32<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 3: k_ar_lsa32<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 4: k_ar_lsa32<4><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 5: k_ar_lsa32<5><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 6: k_ar_lsa32<6><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 7: k_ar_lsa32<7><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 8: k_ar_lsa32<8><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
+        }
+        CKL("k_ar_lsa32");
         return SMPU_OK;
     }
     switch (ctx->world) {
@@ -745,7 +760,14 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         ctx->ar_impl = SMPU_AR_NCCL;
         if (ctx->acc_from_nccl) {
             // symmetric window over the accumulator + device communicator with one LSA barrier per CTA
-            ctx->grid_ar = prop.multiProcessorCount * 2;
+            {
+                // one CTA per SM with 256-bit peer accesses: measured best at W = 2 and 4 (fewer CTAs starve
+                // NVLink, more steal issue slots and HBM from the concurrent K1 / K2); env overrides for tuning
+                const char* ea = getenv("SMPU_AR_CTAS");
+                ctx->grid_ar = ea && atoi(ea) > 0 ? atoi(ea) : prop.multiProcessorCount;
+                const char* vv = getenv("SMPU_AR_VEC32");
+                ctx->ar_vec32 = vv ? atoi(vv) != 0 : true;
+            }
             r = cudaMemset((char*)ctx->acc + ctx->dec_area_off, 0, win_bytes - ctx->dec_area_off) == cudaSuccess
                     ? ncclSuccess
                     : ncclUnhandledCudaError;
