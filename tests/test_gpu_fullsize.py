@@ -147,3 +147,48 @@ def test_big_enfr_5200_updates_periodic_overflow(P, gold):
     check_state(gpu_state(step, idx), snapshot(orc), mags, RTOL_100, where="after 5200 updates")
     s = step.scalars()
     assert (s["e"], s["clean"], s["t"], s["attempts"]) == (1, 197, 5192, 5200)
+
+
+def test_more_than_2_31_elements(P):
+    """Maximum-size edge: a 2^31 + 2^20 + 9 element vector (64-bit indexing in every kernel, 43 GB of HBM),
+    odd tensor sizes so the last buckets start unaligned; sampled parity incl. elements beyond 2^31, a skip."""
+    import torch
+    n_big = (1 << 31) + (1 << 20) + 9
+    tensors = [("w0", (1 << 30) + 3, 0), ("b0", 1001, 1), ("w1", n_big - ((1 << 30) + 3) - 1001 - 4097, 0),
+               ("e", 4097, 2)]
+    inj = [dict(u=2, kind="NINF", r=0, k=2, i=(1 << 31) + 12345)]
+    wl = models.Workload("huge", tensors, 1, 2, injections=inj)
+    lay = synth.Layout(wl)
+    assert lay.n == n_big
+    theta0 = torch.empty(lay.n, dtype=torch.float32, device="cuda")
+    synth.theta0_gpu(theta0, wl)
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=1 << 30))
+    del theta0
+    torch.cuda.empty_cache()
+    idx = _sample_idx(lay, step.bucket_begin, extra=[(1 << 31) - 1, 1 << 31, (1 << 31) + 12345, lay.n - 1],
+                      n_random=2048)
+    orc = O.Oracle(synth.theta0_sample(wl, idx))
+    mags = Magnitudes(orc.theta.copy())
+    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(2)]
+    for u in (1, 2, 3):
+        e = orc.e
+        _gpu_inputs(wl, lay, u, 0, e, bufs)
+        toks = [synth.ntokens(wl, u, 0, k) for k in (1, 2)]
+        step.accumulate(bufs[0], toks[0])
+        step.accumulate(bufs[1], toks[1])
+        res = step.step()
+        grads = [[synth.micro_grad_sample(wl, lay, idx, u, 0, k, e) for k in (1, 2)]]
+        before = orc.theta.copy()
+        ores = orc.update(grads, [toks], overflow=(u == 2))
+        assert decisions(res) == oracle_decisions(ores), (u, res, ores)
+        if ores["applied"]:
+            mags.update(ores["R"], ores["e_used"], ores["N"], before, orc.theta)
+        sel = torch.from_numpy(idx).cuda()
+        gpu = {}
+        for name, which in (("theta", P.smpu.STATE_MASTER), ("m", P.smpu.STATE_M), ("v", P.smpu.STATE_V),
+                            ("w16", P.smpu.STATE_W16)):
+            full = step.get_state(which)
+            gpu[name] = full[idx]
+            del full
+        check_state(gpu, snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
+        del sel
