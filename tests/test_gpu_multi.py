@@ -86,3 +86,15 @@ def test_c3_enfr_5200_updates_world4():
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
     print(p.stdout[-3000:], p.stderr[-3000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_world_invariance_bitwise(world):
+    """(W, c=1) through the fused all-reduce == (1, c=W) locally, bit for bit, with G_real (SURVEY c.3)."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29560 + world), "tests/mp_world_invariance_worker.py"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    print(p.stdout[-3000:], p.stderr[-3000:])
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]

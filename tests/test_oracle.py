@@ -328,6 +328,26 @@ def test_world_and_accumulation_equivalence_exact_family():
                 assert np.array_equal(a, b), (W, c)
 
 
+def test_one_rank_many_micro_equals_many_ranks_one_micro_real_values():
+    # SURVEY c.3: with G_real (order-dependent values) only (W=1, c) == (W=c, 1) holds bitwise -- the same
+    # association: ((g1 + g2) + g3) + g4 locally, or ascending-rank ((A0 + A1) + A2) + A3.
+    base = models.Workload("t", [("w", 20_000, 0), ("e", 999, 2)], 1, 4)
+    lay = synth.Layout(base)
+    micro = [synth.micro_grad_cpu(base, lay, 1, 0, k, 7) for k in range(1, 5)]
+    states = []
+    for W, c in ((1, 4), (4, 1)):
+        orc = O.Oracle(synth.theta0_cpu(base, lay))
+        orc.update([[micro[r * c + k] for k in range(c)] for r in range(W)], [[10] * c for _ in range(W)])
+        states.append((orc.theta, orc.m, orc.v, orc.w16))
+    for a, b in zip(*states):
+        assert np.array_equal(a, b)
+    # and a regrouping with a different association is NOT bitwise in general (SPEC S:633's claim is false)
+    orc = O.Oracle(synth.theta0_cpu(base, lay))
+    res = orc.update([[micro[0], micro[1]], [micro[2], micro[3]]], [[10, 10], [10, 10]])
+    ref = O.reduce([O.accumulate(micro)])
+    assert not np.array_equal(res["R"], ref)
+
+
 def test_large_batch_gradient_softmax_regression():
     # North star pin: the summed micro-batch gradient equals the single-worker large-batch gradient, and
     # the update divides it once by the global target-token count N.  Brute force on a tiny
