@@ -38,11 +38,18 @@ def build_synth_gpu():
           os.path.join(ROOT, "synth", "synth_gpu.cu"), "-o", os.path.join(ROOT, "synth", "libsynth_gpu.so")])
 
 
+def build_sched():
+    _run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", os.path.join(ROOT, "include"),
+          os.path.join(PKG, "csrc", "sched.cpp"), "-o", os.path.join(PKG, "libsmpu_sched.so")])
+
+
 def build_all():
     build_smpu()
+    build_sched()
     build_synth_gpu()
 
 
 if __name__ == "__main__":
     build_smpu(verbose_ptxas="-v" in sys.argv)
+    build_sched()
     build_synth_gpu()

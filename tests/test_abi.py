@@ -87,3 +87,19 @@ def test_product_has_no_oracle_dependency():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower().replace("oracle-exact", ""), f
+
+
+def test_sched_library_exports_header():
+    so = os.path.join(ROOT, "paper_1806_00187_b200", "libsmpu_sched.so")
+    if not os.path.exists(so):
+        import subprocess
+        import sys
+        subprocess.run([sys.executable, "-c", "from paper_1806_00187_b200 import _build; _build.build_sched()"],
+                       cwd=ROOT, check=True)
+    src = open(os.path.join(ROOT, "include", "smpu_sched.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = sorted(set(re.findall(r"\b(smpu_sched_[a-z_]+)\s*\(", src)))
+    assert len(names) == 5
+    lib = ctypes.CDLL(so)
+    for name in names:
+        assert hasattr(lib, name), name
