@@ -62,6 +62,14 @@ __device__ __forceinline__ void st128(void* p, const V4& v) {
                  : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): `pdl_trigger` lets the next kernel of the stream start its CTAs while
+// this one finishes its last wave; `pdl_wait` blocks until the previous kernel has completed and its memory is
+// visible.  Every kernel below waits before its first dependent load or any store; only loads of data no
+// incomplete kernel writes (the caller's micro-gradient, theta/m/v of the previous update) may precede it.
+// Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // fp16x2 add, round-to-nearest-even, never contracted (reading R1)
 __device__ __forceinline__ uint32_t hadd2_rn(uint32_t a, uint32_t b) {
     uint32_t r;
@@ -194,9 +202,12 @@ __global__ void __launch_bounds__(256, 6) k1_accumulate_1(uint16_t* __restrict__
     const int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
     const int64_t vend = vbeg + nvec * 16;
     uint32_t bad = 0, mx = 0;
+    pdl_trigger();
+    V8 g0;
+    if (tid < nvec) g0 = ld256_ro(gb + vbeg + tid * 16);   // the caller's gradient: no kernel of ours writes it
+    pdl_wait();
     if (tid < nvec) {
         const int64_t i0 = vbeg + tid * 16;
-        V8 g0 = ld256_ro(gb + i0);
         if (!FIRST) {
             V8 a0 = ld256(acc + i0);
 #pragma unroll
@@ -251,6 +262,8 @@ __global__ void __launch_bounds__(256, 4) k1_accumulate_many(uint16_t* __restric
     const int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
     const int64_t vend = vbeg + nvec * 16;
     uint32_t bad = 0, mx = 0;
+    pdl_trigger();
+    pdl_wait();
     if (tid < nvec) {
         const int64_t i0 = vbeg + tid * 16, r0 = i0 - lo;
         V8 x;
@@ -431,6 +444,8 @@ __device__ void decide(int overflow, int64_t N, DevState* st, Scalars* sc, float
 __global__ void k0_decide(int* __restrict__ flag, int64_t tokens, const int64_t* __restrict__ tok_ptr,
                           DevState* __restrict__ st, Scalars* __restrict__ sc, float* __restrict__ loss_scale,
                           smpu_step_result* __restrict__ ring, int ring_mask, DevCfg cfg) {
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (tok_ptr) tokens = *tok_ptr;
     const int overflow = *(volatile int*)flag != 0;
@@ -581,17 +596,26 @@ __global__ void __launch_bounds__(256, 4) k2_adam_1(float* __restrict__ theta, f
                                                     float* __restrict__ v, uint16_t* __restrict__ w16,
                                                     const uint16_t* __restrict__ R, int64_t lo, int64_t hi,
                                                     const Scalars* __restrict__ scp, int32_t need) {
-    if (decision_of(scp) != need) return;
-    const Scalars s = *scp;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     int64_t vbeg = (lo + 7) & ~(int64_t)7;
     if (vbeg > hi) vbeg = hi;
     const int64_t nvec = (hi - vbeg) / 8, vend = vbeg + nvec * 8;
+    pdl_trigger();
+    // theta/m/v were last written by the previous update's Adam, complete before our predecessors could start
+    V8 t0, m0, v0;
+    if (tid < nvec) {
+        const int64_t i0 = vbeg + tid * 8;
+        t0 = ld256(theta + i0);
+        m0 = ld256(m + i0);
+        v0 = ld256(v + i0);
+    }
+    pdl_wait();
+    if (decision_of(scp) != need) return;
+    const Scalars s = *scp;
     if (tid < nvec) {
         const int64_t i0 = vbeg + tid * 8;
         V4 r0 = ld128_ro(R + i0);
-        V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
         V4 w0;
         adam_unit(r0, t0, m0, v0, w0, s);
         st256(theta + i0, t0);

@@ -112,6 +112,7 @@ struct smpu_ctx {
 
     int grid_k1 = 0, grid_k2 = 0, grid_k1s = 0;
     bool k1_oneshot = false, k2_oneshot = false;   // one unit per thread (grid cap "0 CTAs per SM")
+    bool pdl = false;                              // programmatic dependent launch of K1 -> K0 -> K2 (world 1)
 
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -221,6 +222,24 @@ int grid_cap(const char* name, int sms, int default_cps) {
     return cps <= 0 ? 0x7fffffff : sms * cps;
 }
 
+// Launch with programmatic dependent launch (PDL) when enabled: the kernel may start its CTAs while its
+// predecessor in the stream finishes (kernels call pdl_trigger / pdl_wait, kernels.cuh).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(const smpu_ctx* ctx, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ctx->pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 int grid_for(int64_t units, int max_grid) {
     int64_t g = (units + 255) / 256;
     if (g > max_grid) g = max_grid;
@@ -237,15 +256,17 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
         uint16_t* a = ctx->acc;
         int* f = ctx->flag;
         uint32_t* st = ctx->stat;
+        cudaError_t e;
         if (first) {
-            if (stats) k1_accumulate_1<true, false, true><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
-            else if (detect) k1_accumulate_1<true, true, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
-            else k1_accumulate_1<true, false, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+            if (stats) e = launch_pdl(ctx, k1_accumulate_1<true, false, true>, grid, 256, s, a, g, lo, hi, f, st);
+            else if (detect) e = launch_pdl(ctx, k1_accumulate_1<true, true, false>, grid, 256, s, a, g, lo, hi, f, st);
+            else e = launch_pdl(ctx, k1_accumulate_1<true, false, false>, grid, 256, s, a, g, lo, hi, f, st);
         } else {
-            if (stats) k1_accumulate_1<false, false, true><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
-            else if (detect) k1_accumulate_1<false, true, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
-            else k1_accumulate_1<false, false, false><<<grid, 256, 0, s>>>(a, g, lo, hi, f, st);
+            if (stats) e = launch_pdl(ctx, k1_accumulate_1<false, false, true>, grid, 256, s, a, g, lo, hi, f, st);
+            else if (detect) e = launch_pdl(ctx, k1_accumulate_1<false, true, false>, grid, 256, s, a, g, lo, hi, f, st);
+            else e = launch_pdl(ctx, k1_accumulate_1<false, false, false>, grid, 256, s, a, g, lo, hi, f, st);
         }
+        if (e != cudaSuccess) return fail_cuda(ctx, e, "k1_accumulate_1", __LINE__);
     } else if (stats) {
         if (first) k1_accumulate<true, false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag, ctx->stat);
         else k1_accumulate<false, false, true><<<grid, 256, 0, s>>>(ctx->acc, g, lo, hi, ctx->flag, ctx->stat);
@@ -293,7 +314,11 @@ smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaS
         k2_adam<<<grid_for((hi - lo + 7) / 8, ctx->grid_k1s), 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16,
                                                                             ctx->acc, lo, hi, ctx->sc, need);
     } else if (ctx->k2_oneshot)
-        k2_adam_1<<<grid, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, lo, hi, ctx->sc, need);
+    {
+        cudaError_t e = launch_pdl(ctx, k2_adam_1, grid, 256, s, ctx->theta, ctx->m, ctx->v, ctx->w16,
+                                   (const uint16_t*)ctx->acc, lo, hi, (const Scalars*)ctx->sc, need);
+        if (e != cudaSuccess) return fail_cuda(ctx, e, "k2_adam_1", __LINE__);
+    }
     else
         k2_adam<<<grid, 256, 0, s>>>(ctx->theta, ctx->m, ctx->v, ctx->w16, ctx->acc, lo, hi, ctx->sc, need);
     CKL("k2_adam");
@@ -719,6 +744,10 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_adam, 256, 0));
     ctx->grid_k2 = grid_cap("SMPU_K2_CTAS_PER_SM", prop.multiProcessorCount, 0);
     ctx->k2_oneshot = ctx->grid_k2 == 0x7fffffff;
+    {
+        const char* pv = getenv("SMPU_PDL");
+        ctx->pdl = world == 1 && (pv ? atoi(pv) != 0 : true);
+    }
     IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1s_sweep, 256, 0));
     ctx->grid_k1s = prop.multiProcessorCount * (occ > 0 ? occ : 1);
 
@@ -1080,8 +1109,9 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     } else {
         {
             Timed t(ctx, SMPU_K0, s);
-            k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->local_tokens, tok_src(ctx), ctx->st, ctx->sc, ctx->scale,
-                                       ctx->ring_dev, kRing - 1, ctx->dcfg);
+            cudaError_t e = launch_pdl(ctx, k0_decide, 1, 32, s, ctx->flag, ctx->local_tokens, tok_src(ctx), ctx->st,
+                                       ctx->sc, ctx->scale, ctx->ring_dev, (int)(kRing - 1), ctx->dcfg);
+            if (e != cudaSuccess) return fail_cuda(ctx, e, "k0_decide", __LINE__);
             CKL("k0_decide");
         }
         {
