@@ -17,7 +17,7 @@ def P():
     if not os.path.exists(so):
         import subprocess
         import sys
-        subprocess.run([sys.executable, "-m", "paper_1806_00187_b200._build"], cwd=ROOT, check=True)
+        subprocess.run([sys.executable, os.path.join("paper_1806_00187_b200", "_build.py")], cwd=ROOT, check=True)
     import paper_1806_00187_b200 as pkg
     return pkg
 
@@ -94,8 +94,7 @@ def test_sched_library_exports_header():
     if not os.path.exists(so):
         import subprocess
         import sys
-        subprocess.run([sys.executable, "-c", "from paper_1806_00187_b200 import _build; _build.build_sched()"],
-                       cwd=ROOT, check=True)
+        subprocess.run([sys.executable, os.path.join("paper_1806_00187_b200", "_build.py")], cwd=ROOT, check=True)
     src = open(os.path.join(ROOT, "include", "smpu_sched.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = sorted(set(re.findall(r"\b(smpu_sched_[a-z_]+)\s*\(", src)))

@@ -14,8 +14,7 @@ def S():
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if not os.path.exists(os.path.join(root, "paper_1806_00187_b200", "libsmpu_sched.so")):
-        subprocess.run([sys.executable, "-c", "from paper_1806_00187_b200 import _build; _build.build_sched()"],
-                       cwd=root, check=True)
+        subprocess.run([sys.executable, os.path.join("paper_1806_00187_b200", "_build.py")], cwd=root, check=True)
     from paper_1806_00187_b200 import sched
     return sched
 
