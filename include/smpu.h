@@ -157,6 +157,13 @@ smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16);
  * host round trip. */
 smpu_status smpu_loss_scale(const smpu_ctx* ctx, const float** dev_scale);
 
+/* The fp16[n] accumulator itself (device, library-owned, valid until smpu_destroy), for producers that add
+ * their weight gradients in place -- e.g. a cuBLAS dW GEMM with beta = 0 for the first micro-batch of an
+ * update and beta = 1 after it -- and then declare the micro-batch with micro_grads = NULL below.
+ * The result is the producer's: cuBLAS's fp16 epilogue was measured to compute rn16(rn16(dW) + A), the same
+ * two roundings as K1 (reading R1; tests/test_gpu_parity.py), but a GEMM that rounds once would differ. */
+smpu_status smpu_accumulator(const smpu_ctx* ctx, void** dev_acc);
+
 /* One whole micro-batch.  micro_grads: host or device fp16[n] (bit patterns), packed; device buffers
  * should be 32-byte aligned for the vector path (any 2-byte alignment is correct).  Gradients are those
  * of the SCALED token-SUM loss of the micro-batch (reading R11).  ntokens >= 0: its non-pad target
@@ -172,6 +179,10 @@ smpu_status smpu_accumulate(smpu_ctx* ctx, const void* micro_grads, int64_t ntok
  * DEVICE fp16[n]; ntokens[k] >= 0; 1 <= count <= 32 and count <= micro-batches left in the update. */
 smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* micro_grads, const int64_t* ntokens, int count,
                                  void* stream);
+
+/* micro_grads == NULL (here and in smpu_accumulate_bucket): the producer already accumulated this micro-batch
+ * (or bucket) into smpu_accumulator in place, stream-ordered before this call on `stream`; the library only
+ * counts it and, on the last micro-batch, runs the overflow test / statistic and the bucket all-reduces. */
 
 /* Bucket-wise micro-batch, for overlap with a still-running backward: micro_begin, then
  * exactly one accumulate_bucket per bucket in any order (buckets are all-reduced in canonical bucket

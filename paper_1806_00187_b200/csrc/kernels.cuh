@@ -314,6 +314,37 @@ __global__ void __launch_bounds__(256, 4) k1_accumulate_many(uint16_t* __restric
     if (STATS) publish_max(mx, stat);
 }
 
+// Scan of the accumulator itself, for micro-batches the producer accumulated in place (a weight-
+// gradient GEMM adding its output into smpu_accumulator with beta = 1): the overflow test (W = 1) or the max
+// |A| statistic (W > 1) that K1 would have fused, 2 bytes per element, one-shot.
+template <bool DETECT, bool STATS>
+__global__ void __launch_bounds__(256) k1_scan(const uint16_t* __restrict__ acc, int64_t lo, int64_t hi,
+                                               int* __restrict__ flag, uint32_t* __restrict__ stat) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    const int64_t nvec = (hi - vbeg) / 16, vend = vbeg + nvec * 16;
+    uint32_t bad = 0, mx = 0;
+    if (tid < nvec) {
+        V8 a = ld256_ro(acc + vbeg + tid * 16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (DETECT) bad |= nonfinite_bits(a.w[j]);
+            if (STATS) mx = mag_max2(mx, a.w[j]);
+        }
+    }
+    auto elem = [&](int64_t i) {
+        uint16_t x = acc[i];
+        if (DETECT && h_nonfinite(x)) bad |= 1u;
+        if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+    };
+    for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+    for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    if (DETECT) raise_flag(bad != 0, flag);
+    if (STATS) publish_max(mx, stat);
+}
+
 // ---------------------------------------------------------------------------------------------- K1s
 struct Scalars;
 __device__ __forceinline__ int32_t decision_of(const Scalars* sc);

@@ -328,6 +328,17 @@ smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaS
 // accumulate src (host or device) into acc[lo, hi)
 smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, bool first, bool detect,
                              cudaStream_t s, bool stats = false) {
+    if (!src) {
+        // accumulated in place by the producer (smpu_accumulator): only the last micro-batch's
+        // overflow test / statistic remains to be done
+        if ((!detect && !stats) || hi <= lo) return SMPU_OK;
+        int grid = grid_for((hi - lo + 15) / 16, 0x7fffffff);
+        Timed t(ctx, SMPU_K1S, s);
+        if (stats) k1_scan<false, true><<<grid, 256, 0, s>>>(ctx->acc, lo, hi, ctx->flag, ctx->stat);
+        else k1_scan<true, false><<<grid, 256, 0, s>>>(ctx->acc, lo, hi, ctx->flag, ctx->stat);
+        CKL("k1_scan");
+        return SMPU_OK;
+    }
     if (classify(src) == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s, stats);
     // host memory: double-buffered H2D staging on the copy stream, overlapped with K1 on `s`
     for (int64_t c0 = lo; c0 < hi; c0 += kStageElems) {
@@ -892,6 +903,12 @@ smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_be
     return SMPU_OK;
 }
 
+smpu_status smpu_accumulator(const smpu_ctx* ctx, void** dev_acc) {
+    if (!ctx || !dev_acc) return set_err(SMPU_EINVAL, "null argument");
+    *dev_acc = ctx->acc;
+    return SMPU_OK;
+}
+
 smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16) {
     if (!ctx || !dev_w16) return set_err(SMPU_EINVAL, "null argument");
     *dev_w16 = ctx->w16;
@@ -922,7 +939,6 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
     LIVE(ctx);
     if (!ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_accumulate_bucket without smpu_micro_begin");
     if (bucket < 0 || bucket >= ctx->nb) return set_err(SMPU_EINVAL, "bucket %d out of [0, %d)", bucket, ctx->nb);
-    if (!grads) return set_err(SMPU_EINVAL, "null grads");
     if (ctx->bucket_done[bucket]) return set_err(SMPU_ESTATE, "bucket %d already given in this micro-batch", bucket);
     CK(cudaSetDevice(ctx->dev));
     cudaStream_t s = (cudaStream_t)stream;
@@ -951,7 +967,6 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
 
 smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, void* stream) {
     LIVE(ctx);
-    if (!grads) return set_err(SMPU_EINVAL, "null grads");
     if (ntokens < 0) return set_err(SMPU_EINVAL, "ntokens < 0");
     if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "a bucket-wise micro-batch is open");
     if (ctx->micro >= ctx->cfg.update_freq)
@@ -965,7 +980,7 @@ smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, v
         if (st != SMPU_OK) return st;
         const uint16_t* g = (const uint16_t*)grads;
         for (int b = 0; b < ctx->nb; ++b) {
-            st = smpu_accumulate_bucket(ctx, b, g + ctx->bbegin[b], stream);
+            st = smpu_accumulate_bucket(ctx, b, g ? g + ctx->bbegin[b] : nullptr, stream);
             if (st != SMPU_OK) return st;
         }
         return SMPU_OK;

@@ -52,7 +52,7 @@ class StepResult(ctypes.Structure):
 
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
-           "smpu_num_params", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
+           "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
            "smpu_accumulate_many", "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_graph_capture", "smpu_graph_launch",
            "smpu_result", "smpu_get_master",
            "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace",
@@ -82,6 +82,7 @@ def lib():
             "smpu_shard_ranges": ([p, p, i32, P(ctypes.c_int)], st),
             "smpu_buckets": ([p, P(ctypes.c_int), p], st),
             "smpu_weights_fp16": ([p, P(p)], st),
+            "smpu_accumulator": ([p, P(p)], st),
             "smpu_loss_scale": ([p, P(p)], st),
             "smpu_accumulate": ([p, p, i64, p], st),
             "smpu_micro_begin": ([p, i64], st),
@@ -252,6 +253,13 @@ class UpdateStep:
     def weights_fp16_ptr(self) -> int:
         p = ctypes.c_void_p()
         _check(lib().smpu_weights_fp16(self._ctx, ctypes.byref(p)))
+        return p.value
+
+    def accumulator_ptr(self) -> int:
+        """Device pointer of the fp16[n] accumulator, for producers that accumulate in place (then pass
+        micro_grads=None to accumulate / accumulate_bucket)."""
+        p = ctypes.c_void_p()
+        _check(lib().smpu_accumulator(self._ctx, ctypes.byref(p)))
         return p.value
 
     def loss_scale_ptr(self) -> int:

@@ -25,6 +25,11 @@ from tests.gpu_util import (RTOL_1, Magnitudes, check_state, decisions, gpu_stat
                             oracle_decisions, snapshot)
 
 
+class _AccView:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f2", "data": (ptr, False), "version": 3}
+
+
 def main():
     family = sys.argv[1] if len(sys.argv) > 1 else "exact"
     updates = int(sys.argv[2]) if len(sys.argv) > 2 else 8
@@ -32,6 +37,7 @@ def main():
     use_graph = len(sys.argv) > 4 and sys.argv[4] == "graph"
     sharded = len(sys.argv) > 4 and sys.argv[4] == "sharded"
     many = len(sys.argv) > 4 and sys.argv[4] == "many"
+    external = len(sys.argv) > 4 and sys.argv[4] == "external"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -95,6 +101,13 @@ def main():
                 gbufs[k].copy_(torch.from_numpy(mine[k].view(np.int16)))
             step.graph_launch(toks)
             res = step.result(u)
+        elif external:     # the producer accumulates in place (torch fp16 copy/add), declares with None
+            acc = torch.as_tensor(_AccView(step.accumulator_ptr(), lay.n), device="cuda")
+            for k in range(c):
+                g = h2t(mine[k]).view(torch.float16)
+                acc.copy_(g) if k == 0 else acc.add_(g)
+                step.accumulate(None, toks[k])
+            res = step.step()
         elif many:     # resident micro-batches: the first one alone, then the rest (incl. the final) in one pass
             step.accumulate(h2t(mine[0]), toks[0])
             step.accumulate_many([h2t(x) for x in mine[1:]], toks[1:])
@@ -168,7 +181,8 @@ def main():
     if rank == 0:
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
               f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
-              f"{' + sharded optimizer bitwise' if sharded else ''}{' via accumulate_many' if many else ''}")
+              f"{' + sharded optimizer bitwise' if sharded else ''}{' via accumulate_many' if many else ''}"
+              f"{' with in-place producer accumulation' if external else ''}")
 
 
 if __name__ == "__main__":

@@ -14,11 +14,12 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False, many=False):
+def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False, many=False,
+         external=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
            str(updates), impl] + (["graph"] if graph else []) + (["sharded"] if sharded else []) + \
-          (["many"] if many else [])
+          (["many"] if many else []) + (["external"] if external else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
@@ -38,6 +39,13 @@ def test_world2_cuda_graph(impl):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, "real", port=29535 + (impl == "fused"), impl=impl, graph=True)
+
+
+def test_world2_external_accumulation():
+    """In-place producer accumulation (smpu_accumulator + micro_grads=None) at W = 2: scans + all-reduces."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "real", port=29538, impl="fused", external=True)
 
 
 def test_world2_accumulate_many_final_microbatch():

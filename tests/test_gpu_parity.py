@@ -312,3 +312,80 @@ def test_accumulate_many_bitwise_equals_streaming(P):
     with pytest.raises(P.SmpuError) as ei:
         b.accumulate_many(dev + [dev[0]], toks + [1])     # 6 micro-batches with update_freq 5
     assert ei.value.status == P.smpu.ESTATE
+
+
+class _DevView:
+    """A library-owned device array viewed (not copied) by torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr, n, typestr="<f2"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+def test_external_accumulation_bitwise(P):
+    """SURVEY f3 contract: the producer adds its micro-gradients into smpu_accumulator in place (here torch fp16
+    copy/add: rn16(fp32(a)+fp32(b)) == rn16(a+b), innocuous double rounding) and declares them with
+    micro_grads=None; the update equals the library-accumulated one bit for bit, decisions the oracle's."""
+    import torch
+    tensors = [("a", 17, 1), ("b", 100_003, 0), ("c", 65_536, 2)]
+    wl = models.Workload("ext", tensors, 1, 3, injections=[dict(u=2, kind="NAN", r=0, k=2, i=50)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    x = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=100_000))
+    acc = torch.as_tensor(_DevView(x.accumulator_ptr(), lay.n), device="cuda")
+    orc = O.Oracle(theta0)
+    for u in range(1, 5):
+        e = orc.e
+        grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in (1, 2, 3)]
+        toks = [synth.ntokens(wl, u, 0, k) for k in (1, 2, 3)]
+        ores = orc.update([grads], [toks])
+        for k in range(3):
+            g = h2t(grads[k]).view(torch.float16)
+            a.accumulate(g.view(torch.int16), toks[k])
+            if k == 0:
+                acc.copy_(g)
+            else:
+                acc.add_(g)
+            if k < 2:
+                x.accumulate(None, toks[k])
+            else:                                   # the last one bucket by bucket, as a backward would
+                x.micro_begin(toks[k])
+                for b in reversed(range(x.n_buckets)):
+                    x.accumulate_bucket(b, None)
+        ra, rx = a.step(), x.step()
+        assert decisions(ra) == decisions(rx) == oracle_decisions(ores), u
+        for w in (0, 1, 2, 3, 4, 5):
+            assert np.array_equal(a.get_state(w), x.get_state(w)), (u, w)
+
+
+def test_external_gemm_epilogue_accumulation(P):
+    """The f3 producer: dW = dY^T X by cuBLAS with beta = 1 straight into the accumulator.  Measured on B200,
+    cuBLAS's fp16 epilogue computes rn16(rn16(alpha * dW_fp32) + A), i.e. the paper's two roundings (reading R1):
+    the in-place update is bitwise the same as the GEMM into a scratch buffer followed by the library's K1
+    (a second ctx), and both finish identically."""
+    import torch
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False   # fp32 accumulation in cuBLAS
+    out_f, in_f, T = 384, 256, 3000
+    wl = models.Workload("gemm", [("w", out_f * in_f, 0)], 1, 4)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    x = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    y = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    acc = torch.as_tensor(_DevView(x.accumulator_ptr(), lay.n), device="cuda").view(out_f, in_f)
+    scratch = torch.empty(out_f, in_f, dtype=torch.float16, device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    for u in range(1, 3):
+        for k in range(4):
+            dy = (torch.randn(T, out_f, device="cuda", generator=gen) * 0.05).half()
+            xx = (torch.randn(T, in_f, device="cuda", generator=gen) * 0.05).half()
+            # in place: beta = 0 for the first micro-batch of the update, 1 after; alpha = the loss scale 2^7
+            torch.addmm(acc, dy.t(), xx, beta=0.0 if k == 0 else 1.0, alpha=2.0**7, out=acc)
+            x.accumulate(None, T)
+            torch.addmm(scratch, dy.t(), xx, beta=0.0, alpha=2.0**7, out=scratch)
+            y.accumulate(scratch.view(-1).view(torch.int16), T)
+            torch.cuda.synchronize()
+            assert np.array_equal(x.get_state(P.smpu.STATE_ACCUM), y.get_state(P.smpu.STATE_ACCUM)), (u, k)
+        rx, ry = x.step(), y.step()
+        assert decisions(rx) == decisions(ry) and rx["applied"] == 1 and rx["ntokens_total"] == 4 * T
+        for w in (0, 1, 2, 3):
+            assert np.array_equal(x.get_state(w), y.get_state(w)), (u, w)
