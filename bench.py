@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="time the call-by-call path (c x smpu_accumulate + smpu_step) instead of the captured "
                          "CUDA graph of the same update (smpu_graph_capture / smpu_graph_launch)")
+    ap.add_argument("--m2-fused", action="store_true",
+                    help="M2 with SURVEY f3's producer: dW GEMMs accumulate in place into smpu_accumulator "
+                         "(cuBLAS beta = 1; bitwise the paper's accumulate), 1-D tensors by fp16 add, no K1")
     ap.add_argument("--trace", default=None, help="write the timed launches (per stream) as JSONL here")
     ap.add_argument("--mode", choices=["m1", "m2"], default="m1",
                     help="m1: the update step alone (headline); m2: with a cuBLAS backward-load emulator so the "
@@ -234,8 +237,18 @@ class BackwardEmulator:
         self.dw = torch.empty(max(o * i for _, o, i, _ in self.mats), device=device, dtype=torch.float16)
         self.n_tensors = len(wl.tensors)
         self.flops_per_token = 6 * sum(o * i for _, o, i, _ in self.mats)
+        self.offsets = np.concatenate([[0], np.cumsum(wl.numel)])
+        # 1-D tensors (biases, LayerNorm) of the in-place producer: one indexed fp16 add per micro-batch
+        mat_ids = {j for j, _, _, _ in self.mats}
+        idx = [np.arange(self.offsets[j], self.offsets[j + 1]) for j in range(len(wl.tensors)) if j not in mat_ids]
+        self.idx1d = torch.from_numpy(np.concatenate(idx).astype(np.int64)).to(device)
+        # issued right before the first bucket boundary, so that every bucket is complete when announced
+        self.first_1d_ready = min(self.bucket_of_end) if self.bucket_of_end else 0
+        self.vec1d = torch.randn(self.idx1d.numel(), device=device, dtype=torch.float16) * 0.01
 
-    def micro(self, T, on_bucket=None):
+    def micro(self, T, on_bucket=None, acc=None, first=False):
+        """acc (the library's accumulator viewed as fp16[n]): accumulate in place instead of into scratch --
+        dW GEMMs with beta = 0 (first micro-batch of the update) or 1, 1-D tensors by fp16 copy / add."""
         import torch
         x, dy = self.x[:T], self.dy[:T]
         for j, o, i, W in reversed(self.mats):                       # forward: reverse ready order
@@ -245,7 +258,14 @@ class BackwardEmulator:
             if j in by_tensor:
                 o, i, W = by_tensor[j]
                 torch.mm(dy[:, :o], W, out=self.out[:T * i].view(T, i))                    # dX
-                torch.mm(dy[:, :o].t(), x[:, :i], out=self.dw[:o * i].view(o, i))          # dW
+                if acc is not None:
+                    dst = acc[self.offsets[j]:self.offsets[j + 1]].view(o, i)
+                    torch.addmm(dst, dy[:, :o].t(), x[:, :i], beta=0.0 if first else 1.0, out=dst)
+                else:
+                    torch.mm(dy[:, :o].t(), x[:, :i], out=self.dw[:o * i].view(o, i))      # dW
+            if acc is not None and j == self.first_1d_ready:
+                # every 1-D tensor's gradient at once (they are tiny): copy or fp16 add at their indices
+                acc.index_copy_(0, self.idx1d, self.vec1d) if first else acc.index_add_(0, self.idx1d, self.vec1d)
             if on_bucket is not None and j in self.bucket_of_end:
                 on_bucket(self.bucket_of_end[j])
 
@@ -258,12 +278,26 @@ def run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg,
     def emulator_for(st):
         return BackwardEmulator(wl, st.weights_fp16_ptr(), st.bucket_begin, f"cuda:{local}")
 
+    class _Acc:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f2", "data": (ptr, False), "version": 3}
+
     def one(st, emu):
+        bb = st.bucket_begin
+        if args.m2_fused:      # the backward accumulates in place; the library is told with None
+            acc = torch.as_tensor(_Acc(st.accumulator_ptr(), lay.n), device=f"cuda:{local}")
+            for k in range(c - 1):
+                emu.micro(toks[k], acc=acc, first=(k == 0))
+                st.accumulate(None, toks[k], stream)
+            st.micro_begin(toks[c - 1])
+            emu.micro(toks[c - 1], on_bucket=lambda b: st.accumulate_bucket(b, None, stream), acc=acc,
+                      first=(c == 1))
+            st.step(stream, wait=False)
+            return
         for k in range(c - 1):
             emu.micro(toks[k])
             st.accumulate(grads[k], toks[k], stream)
         st.micro_begin(toks[c - 1])
-        bb = st.bucket_begin
         emu.micro(toks[c - 1], on_bucket=lambda b: st.accumulate_bucket(b, grads[c - 1][bb[b]:bb[b + 1]], stream))
         st.step(stream, wait=False)
 
@@ -295,14 +329,17 @@ def run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg,
         s1.close()
     if rank != 0:
         return None
+    tok_per_update = world * sum(toks)
     out = {"metric": METRIC + " (M2: with emulated backward)", "mode": "m2", "n_gpus": world,
+           "producer": "in-place dW-GEMM accumulation (f3)" if args.m2_fused else "separate K1 accumulate",
+           "target_tokens_per_s": tok_per_update / (ms * 1e-3),
            "ms_per_step": ms, "steps": args.steps, "warmup": args.warmup,
            "value": world * c * lay.n / (ms * 1e-3), "unit": UNIT,
            "config": {"workload": wl.name, "update_freq": c, "bucket_mib": args.bucket_mib,
                       "allreduce": {0: None, 1: "nccl", 2: "fused_lsa"}[step.allreduce_impl if world > 1 else 0],
                       "tokens_per_micro": toks, "backward_flops_per_update": emu.flops_per_token * sum(toks)},
-           "update_path_kernels_ms_per_step": stats["k1_add"]["ms"] / args.steps + stats["k1_first"]["ms"] / args.steps
-           + stats["k2_adam"]["ms"] / args.steps,
+           "update_path_kernels_ms_per_step": (stats["k1_add"]["ms"] + stats["k1_first"]["ms"] + stats["k1s_sweep"]["ms"]
+                                               + stats["k2_adam"]["ms"]) / (args.steps + args.warmup),
            "allreduce_ms_per_step": stats["allreduce"]["ms"] / args.steps}
     if ms1 is not None:
         out["exposed_comm"] = {"ms": ms - ms1, "frac_of_update": (ms - ms1) / ms, "t_world1_ms": ms1,
