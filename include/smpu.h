@@ -203,7 +203,8 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out);
  * buffers; their addresses are frozen, their contents are read at replay time) followed by smpu_step into a
  * graph owned by the ctx (replacing any earlier one); flags = SMPU_GRAPH_RESIDENT records one
  * smpu_accumulate_many over all c buffers instead (the producer keeps the c gradients until the replay).
- * It enqueues nothing.  At world > 1 it needs the fused
+ * It enqueues nothing.  With update_freq = 1 at world = 1 the graph tests the buffer for overflow in place and
+ * Adam reads it directly (R = g_1: nothing to copy; the accumulator is then not written by the replays).  At world > 1 it needs the fused
  * all-reduce (EINVAL with SMPU_AR_NCCL).  smpu_graph_launch replays it on
  * `stream` with this update's token counts ntokens[0..c) (host): identical arithmetic and decisions to the
  * call-by-call path, one launch instead of c + 2 (or, at world > 1, the bucket all-reduces, decision and

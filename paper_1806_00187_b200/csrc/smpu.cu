@@ -105,6 +105,8 @@ struct smpu_ctx {
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     bool graph_resident = false;
+    bool graph_direct = false;
+    const uint16_t* k2_src = nullptr;  // captured c = 1, W = 1 graphs: Adam reads the producer's buffer (R = g_1)
     int64_t* tok_dev = nullptr;        // this update's local token count, written before each replay
     int64_t* tok_host = nullptr;       // pinned ring of kRing slots feeding tok_dev
     int64_t attempts = 0;
@@ -315,8 +317,9 @@ smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaS
                                                                             ctx->acc, lo, hi, ctx->sc, need);
     } else if (ctx->k2_oneshot)
     {
-        cudaError_t e = launch_pdl(ctx, k2_adam_1, grid, 256, s, ctx->theta, ctx->m, ctx->v, ctx->w16,
-                                   (const uint16_t*)ctx->acc, lo, hi, (const Scalars*)ctx->sc, need);
+        const uint16_t* R = ctx->k2_src ? ctx->k2_src : ctx->acc;
+        cudaError_t e = launch_pdl(ctx, k2_adam_1, grid, 256, s, ctx->theta, ctx->m, ctx->v, ctx->w16, R, lo, hi,
+                                   (const Scalars*)ctx->sc, need);
         if (e != cudaSuccess) return fail_cuda(ctx, e, "k2_adam_1", __LINE__);
     }
     else
@@ -1174,6 +1177,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
         CK(cudaGraphExecDestroy(ctx->graph_exec));
         ctx->graph_exec = nullptr;
     }
+    ctx->graph_direct = false;
     CK(cudaDeviceSynchronize());
     const bool timing = ctx->timing;
     ctx->timing = false;
@@ -1182,7 +1186,19 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     smpu_status st = SMPU_OK;
     cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
     if (e == cudaSuccess) {
-        if (flags & SMPU_GRAPH_RESIDENT) {
+        if (ctx->cfg.update_freq == 1 && ctx->world == 1 && ctx->k2_oneshot) {
+            // c = 1, W = 1: R = g_1.  The buffer is fixed and read at replay, so nothing needs copying: test it
+            // for overflow in place (2 B/elem) and let Adam read it directly -- 30 instead of 32 B/elem.
+            // (The accumulator, smpu_get_state(ACCUM), is then left untouched by these replays.)
+            Timed t(ctx, SMPU_K1S, ctx->cap_stream);
+            k1_scan<true, false><<<grid_for((ctx->n + 15) / 16, 0x7fffffff), 256, 0, ctx->cap_stream>>>(
+                (const uint16_t*)micro_grads[0], 0, ctx->n, ctx->flag, ctx->stat);
+            cudaError_t el = cudaGetLastError();
+            if (el != cudaSuccess) st = fail_cuda(ctx, el, "k1_scan", __LINE__);
+            start_micro(ctx, 0);
+            ctx->k2_src = (const uint16_t*)micro_grads[0];
+            ctx->graph_direct = true;
+        } else if (flags & SMPU_GRAPH_RESIDENT) {
             std::vector<int64_t> zeros(count, 0);
             st = smpu_accumulate_many(ctx, micro_grads, zeros.data(), count, ctx->cap_stream);
         } else {
@@ -1190,6 +1206,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
                 st = smpu_accumulate(ctx, micro_grads[k], 0, ctx->cap_stream);
         }
         if (st == SMPU_OK) st = smpu_step(ctx, ctx->cap_stream, nullptr);
+        ctx->k2_src = nullptr;
         cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &graph);
         if (e == cudaSuccess) e = e2;
     }
@@ -1205,7 +1222,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
         return st;
     }
     if (e != cudaSuccess) return fail_cuda(ctx, e, "stream capture of the update", __LINE__);
-    ctx->graph_resident = (flags & SMPU_GRAPH_RESIDENT) != 0;
+    ctx->graph_resident = (flags & SMPU_GRAPH_RESIDENT) != 0 && !ctx->graph_direct;
     e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail_cuda(ctx, e, "cudaGraphInstantiate", __LINE__);
@@ -1230,7 +1247,9 @@ smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, 
     if (ctx->attempts >= kRing) CK(cudaEventSynchronize(ctx->ring_ev[slot]));   // slot's previous copy has run
     ctx->tok_host[slot] = N;
     CK(cudaMemcpyAsync(ctx->tok_dev, &ctx->tok_host[slot], sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    if (ctx->graph_resident) {
+    if (ctx->graph_direct) {
+        ctx->launches[SMPU_K1S] += 1;
+    } else if (ctx->graph_resident) {
         ctx->launches[SMPU_K1_MANY] += ctx->world > 1 ? ctx->nb : 1;
     } else {
         ctx->launches[SMPU_K1_FIRST] += 1;

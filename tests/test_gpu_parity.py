@@ -389,3 +389,30 @@ def test_external_gemm_epilogue_accumulation(P):
         assert decisions(rx) == decisions(ry) and rx["applied"] == 1 and rx["ntokens_total"] == 4 * T
         for w in (0, 1, 2, 3):
             assert np.array_equal(x.get_state(w), y.get_state(w)), (u, w)
+
+
+def test_graph_direct_c1_bitwise(P):
+    """update_freq = 1, W = 1 graph: overflow test in place + Adam reading the producer's buffer (no copy) ==
+    the call path bit for bit on theta/m/v/w16 and the decisions, through an injected NaN."""
+    import torch
+    wl = models.Workload("direct", [("w", 200_003, 0), ("b", 9, 1)], 1, 1,
+                         injections=[dict(u=3, kind="NAN", r=0, k=1, i=200_005)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    g = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    orc = O.Oracle(theta0)
+    buf = torch.empty(lay.n, dtype=torch.int16, device="cuda")
+    g.graph_capture([buf])
+    for u in range(1, 6):
+        x = synth.micro_grad_cpu(wl, lay, u, 0, 1, orc.e)
+        tok = synth.ntokens(wl, u, 0, 1)
+        ores = orc.update([[x]], [[tok]])
+        a.accumulate(h2t(x), tok)
+        ra = a.step()
+        buf.copy_(h2t(x))
+        g.graph_launch([tok])
+        rg = g.result(u)
+        assert decisions(ra) == decisions(rg) == oracle_decisions(ores), u
+        for w in (0, 1, 2, 3, 5):
+            assert np.array_equal(a.get_state(w), g.get_state(w)), (u, w)
