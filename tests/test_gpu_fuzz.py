@@ -1,0 +1,95 @@
+"""Randomised parity (hypothesis, fixed seed): random tensor lists (sizes 1..40k, every class), update_freq 1..5,
+bucket thresholds from a few bytes to 1 MiB, every accumulation entry point (whole / bucket-wise in a random
+order / resident accumulate_many / in-place NULL / CUDA graph), injected non-finites anywhere; the library vs the
+oracle on decisions (bitwise), the accumulator (bitwise) and theta/m/v/w16 (tolerance), every update."""
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, seed, settings
+from hypothesis import strategies as st
+
+import oracle as O
+import synth
+from synth import models
+from tests.gpu_util import Magnitudes, check_state, decisions, gpu_state, h2t, lib_cfg, oracle_decisions, snapshot
+
+pytestmark = pytest.mark.gpu
+
+
+class _DevView:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f2", "data": (ptr, False), "version": 3}
+
+
+@st.composite
+def cases(draw):
+    nt = draw(st.integers(1, 6))
+    tensors = [(f"t{j}", draw(st.integers(1, 40_000)), draw(st.integers(0, 2))) for j in range(nt)]
+    c = draw(st.integers(1, 5))
+    n = sum(t[1] for t in tensors)
+    inj = []
+    if draw(st.booleans()):
+        kind = draw(st.sampled_from(["INF", "NINF", "NAN"] + (["ACC_OVF"] if c >= 2 else [])))
+        inj.append(dict(u=draw(st.integers(1, 3)), kind=kind, r=0, k=draw(st.integers(1, c)),
+                        i=draw(st.integers(0, n - 1))))
+    mode = draw(st.sampled_from(["whole", "bucket", "many", "inplace", "graph"]))
+    bucket_bytes = draw(st.sampled_from([2, 1000, 16_384, 100_000, 1 << 20]))
+    order_seed = draw(st.integers(0, 1000))
+    return tensors, c, inj, mode, bucket_bytes, order_seed
+
+
+@seed(20261018)
+@settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck))
+@given(cases())
+def test_fuzz_against_oracle(case):
+    import torch
+    import paper_1806_00187_b200 as P
+    tensors, c, inj, mode, bucket_bytes, order_seed = case
+    wl = models.Workload("fuzz", tensors, 1, c, injections=inj)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=bucket_bytes))
+    orc = O.Oracle(theta0)
+    mags = Magnitudes(theta0)
+    rng = np.random.default_rng(order_seed)
+    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)] if mode == "graph" else None
+    if mode == "graph":
+        step.graph_capture(bufs)
+    acc = torch.as_tensor(_DevView(step.accumulator_ptr(), lay.n), device="cuda") if mode == "inplace" else None
+    for u in range(1, 4):
+        e = orc.e
+        grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in range(1, c + 1)]
+        toks = [synth.ntokens(wl, u, 0, k) for k in range(1, c + 1)]
+        before = snapshot(orc)
+        ores = orc.update([grads], [toks])
+        dev = [h2t(x) for x in grads]
+        if mode == "graph":
+            for k in range(c):
+                bufs[k].copy_(dev[k])
+            step.graph_launch(toks)
+            res = step.result(u)
+        else:
+            if mode == "many":
+                step.accumulate_many(dev, toks)
+            for k in range(c if mode != "many" else 0):
+                if mode == "whole":
+                    step.accumulate(dev[k], toks[k])
+                elif mode == "inplace":
+                    g = dev[k].view(torch.float16)
+                    acc.copy_(g) if k == 0 else acc.add_(g)
+                    step.accumulate(None, toks[k])
+                else:
+                    step.micro_begin(toks[k])
+                    bb = step.bucket_begin
+                    for b in rng.permutation(step.n_buckets):
+                        step.accumulate_bucket(int(b), dev[k][bb[b]:bb[b + 1]])
+            res = step.step()
+        assert decisions(res) == oracle_decisions(ores), (case, u)
+        if mode != "graph" or c > 1:
+            got = step.get_state(P.smpu.STATE_ACCUM)
+            R = ores["R"]
+            fin = (R & 0x7C00) != 0x7C00
+            assert np.array_equal(got[fin], R[fin]) and np.array_equal(got[~fin] & 0x7C00, R[~fin] & 0x7C00)
+        if ores["applied"]:
+            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
+        check_state(gpu_state(step), snapshot(orc), mags, 1e-5, where=f"{case} update {u}")
+    step.close()
