@@ -398,3 +398,33 @@ def test_large_batch_gradient_softmax_regression():
     assert np.all(np.abs(g_oracle - g_true) <= bound)
     # and the normalisation is by N exactly: a wrong divisor (N_r, c, W, or a dropped 2^e) misses by >= 2x
     assert np.abs(g_oracle - g_true).max() < 0.01 * np.abs(g_true).max()
+
+
+def test_c_whole_update_equals_python_driver():
+    # oracle.c's orc_update (the c.1 body in one C call) and the Python driver's step-by-step calls agree
+    import ctypes
+    wl = models.Workload("t", [("w", 5000, 0), ("b", 33, 1)], 3, 2, injections=[dict(u=2, kind="INF", r=1, k=2, i=7)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    py = O.Oracle(theta0)
+    n = lay.n
+    th = theta0.astype(np.float64)
+    m, v = np.zeros(n), np.zeros(n)
+    w16 = O.d2h_array(th)
+    s = O.OrcScaler(7, 0, 0)
+    A = np.empty(3 * n, np.uint16)
+    R = np.empty(n, np.uint16)
+    for u in (1, 2, 3):
+        grads = [[synth.micro_grad_cpu(wl, lay, u, r, k, s.e) for k in (1, 2)] for r in range(3)]
+        toks = [[100 * (r + 1), 50] for r in range(3)]
+        rp = py.update(grads, toks)
+        flat = [g for row in grads for g in row]
+        arr = (ctypes.c_void_p * len(flat))(*[g.ctypes.data for g in flat])
+        res = O.OrcResult()
+        N = sum(sum(t) for t in toks)
+        O.lib().orc_update(O._p(th), O._p(m), O._p(v), O._p(w16), n, arr, 3, 2, N, O._p(A), O._p(R), ctypes.byref(s),
+                           ctypes.byref(O.Config().c()), ctypes.byref(res))
+        assert res.as_dict() == {k: rp[k] for k in res.as_dict()}, u
+        assert np.array_equal(R, rp["R"])
+        assert np.array_equal(th, py.theta) and np.array_equal(m, py.m) and np.array_equal(v, py.v)
+        assert np.array_equal(w16, py.w16)
