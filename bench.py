@@ -448,7 +448,12 @@ def main_ours(args):
     # inside a graph, so the kernel table / roofline above come from the call-by-call region, same kernels
     graph_info = None
     if not args.no_graph:
-        step.graph_capture(grads)
+        try:
+            step.graph_capture(grads)
+        except P.SmpuError as ex:          # e.g. W > 1 fell back to NCCL (not graph-capturable here)
+            print(f"[bench] graph capture unavailable ({ex}); timing the call-by-call path", file=sys.stderr)
+            args.no_graph = True
+    if not args.no_graph:
         for _ in range(args.warmup):
             step.graph_launch(toks, stream)
         torch.cuda.synchronize()
