@@ -584,9 +584,11 @@ def main_ours(args):
                       "achieved_gbs": bytes_total / (st["ms"] * 1e-3) / 1e9}
     dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
     traffic = load_traffic(dom, wl.name)
+    # second denominator for context: ncu's DRAM peak (dram__bytes.sum.peak_sustained 2048 B/cycle x 3.996 GHz)
+    ncu_dram_peak = 2048 * 3.996
     roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["achieved_gbs"], "peak": hbm_peak,
             "unit": "GB/s", "frac": kernels[dom]["achieved_gbs"] / hbm_peak, "peak_source": peak_src,
-            "traffic": traffic}
+            "traffic": traffic, "frac_of_ncu_dram_peak": kernels[dom]["achieved_gbs"] / ncu_dram_peak}
     path_bytes = n * (6 * c - 2 + 28)
     out = {"metric": METRIC, "value": world * c * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
