@@ -1038,6 +1038,28 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const 
     return leave_stream(ctx, s);
 }
 
+smpu_status smpu_allreduce_accumulator(smpu_ctx* ctx, void* stream) {
+    LIVE(ctx);
+    if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_allreduce_accumulator inside an update");
+    if (ctx->world == 1) return SMPU_OK;
+    if (ctx->sharded) return set_err(SMPU_EINVAL, "the sharded ctx reduce-scatters; no all-reduce to run");
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    smpu_status st = enter_stream(ctx, s);
+    if (st != SMPU_OK) return st;
+    for (int b = 0; b < ctx->nb; ++b) {
+        CK(cudaEventRecord(ctx->ready[b], s));
+        ctx->bucket_done[b] = 1;
+    }
+    ctx->next_issue = 0;
+    st = issue_ready_buckets(ctx);
+    std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    ctx->next_issue = 0;
+    if (st != SMPU_OK) return st;
+    CK(cudaStreamWaitEvent(s, ctx->comm_done, 0));
+    return leave_stream(ctx, s);
+}
+
 smpu_status smpu_result(smpu_ctx* ctx, int64_t attempt, smpu_step_result* out) {
     LIVE(ctx);
     if (!out) return set_err(SMPU_EINVAL, "null out");

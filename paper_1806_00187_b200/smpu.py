@@ -52,12 +52,11 @@ class StepResult(ctypes.Structure):
 
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
-           "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets", "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate",
-           "smpu_accumulate_many", "smpu_micro_begin", "smpu_accumulate_bucket", "smpu_step", "smpu_graph_capture", "smpu_graph_launch",
-           "smpu_result", "smpu_get_master",
-           "smpu_get_state", "smpu_set_state", "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace",
-           "smpu_last_error",
-           "smpu_destroy"]
+           "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets",
+           "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate", "smpu_accumulate_many", "smpu_micro_begin",
+           "smpu_accumulate_bucket", "smpu_step", "smpu_allreduce_accumulator", "smpu_graph_capture",
+           "smpu_graph_launch", "smpu_result", "smpu_get_master", "smpu_get_state", "smpu_set_state",
+           "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace", "smpu_last_error", "smpu_destroy"]
 
 _lib = None
 
@@ -90,6 +89,7 @@ def lib():
             "smpu_accumulate_bucket": ([p, i32, p, p], st),
             "smpu_step": ([p, p, P(StepResult)], st),
             "smpu_result": ([p, i64, P(StepResult)], st),
+            "smpu_allreduce_accumulator": ([p, p], st),
             "smpu_graph_capture": ([p, p, i32, i32], st),
             "smpu_graph_launch": ([p, p, i32, p], st),
             "smpu_get_master": ([p, p, i64], st),
@@ -225,6 +225,9 @@ class UpdateStep:
     def graph_launch(self, ntokens, stream=None):
         toks = np.ascontiguousarray(ntokens, dtype=np.int64)
         _check(lib().smpu_graph_launch(self._ctx, _ptr(toks), toks.size, _stream(stream)))
+
+    def allreduce_accumulator(self, stream=None):
+        _check(lib().smpu_allreduce_accumulator(self._ctx, _stream(stream)))
 
     def result(self, attempt: int):
         r = StepResult()

@@ -106,3 +106,16 @@ def test_world_invariance_bitwise(world):
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-3000:], p.stderr[-3000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("impl", ["fused", "nccl"])
+def test_allreduce_accumulator_primitive(impl):
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = 4 if _ngpu() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29570 + (impl == "nccl")), "tests/mp_allreduce_worker.py",
+           impl]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    print(p.stdout[-3000:], p.stderr[-3000:])
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
