@@ -416,3 +416,19 @@ def test_graph_direct_c1_bitwise(P):
         assert decisions(ra) == decisions(rg) == oracle_decisions(ores), u
         for w in (0, 1, 2, 3, 5):
             assert np.array_equal(a.get_state(w), g.get_state(w)), (u, w)
+
+
+def test_real_training_loop_example(P):
+    """examples/train_tiny.py: a real fp16 model whose weights are views of the library's w16, loss scaled by the
+    library's device scale, update by libsmpu -- the loss must fall from ln V towards the 10%-noise floor."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "train_tiny", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples",
+                                   "train_tiny.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    losses, scales = mod.run(updates=120, verbose=False)
+    assert losses[0] > 3.5                      # ~ ln 64 = 4.16 at init
+    assert np.mean(losses[-10:]) < 1.5         # learned (noise floor ~0.1*ln 64 + entropy terms)
+    assert all(-5 <= s <= 24 for s in scales)
