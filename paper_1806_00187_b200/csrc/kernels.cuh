@@ -22,6 +22,10 @@
 
 #include "smpu.h"
 
+#ifndef SMPU_K1_MINB
+#define SMPU_K1_MINB 6   // min resident CTAs/SM for the one-shot K1 (register cap 40); 8 forces 32 registers
+#endif
+
 namespace smpu {
 
 struct __align__(32) V8 { uint32_t w[8]; };   // 32 B: 16 halves or 8 floats
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
 // (tools/hbm_probe.cu: 2R1W one-shot 6.3-6.8 TB/s vs 6.2 for the 4-CTA/SM persistent loop).  The element
 // path (unaligned head / tail / not co-aligned) is taken by the first threads of the grid.
 template <bool FIRST, bool DETECT, bool STATS>
-__global__ void __launch_bounds__(256, 6) k1_accumulate_1(uint16_t* __restrict__ acc, const uint16_t* __restrict__ g,
+__global__ void __launch_bounds__(256, SMPU_K1_MINB) k1_accumulate_1(uint16_t* __restrict__ acc, const uint16_t* __restrict__ g,
                                                           int64_t lo, int64_t hi, int* __restrict__ flag,
                                                           uint32_t* __restrict__ stat) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
