@@ -184,6 +184,13 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* micro_grads, 
  * (or bucket) into smpu_accumulator in place, stream-ordered before this call on `stream`; the library only
  * counts it and, on the last micro-batch, runs the overflow test / statistic and the bucket all-reduces. */
 
+/* Per-tensor ready hook for in-place producers ("when the gradient computation for a layer
+ * finishes, we add the result to a synchronization buffer"): after smpu_micro_begin, call it once per tensor
+ * (gradient-ready index, as given to smpu_init) when that tensor's gradient is in smpu_accumulator; when the
+ * last tensor of a bucket is in, the bucket is handed over exactly as smpu_accumulate_bucket(b, NULL).
+ * ESTATE on a repeated tensor or a bucket already given whole. */
+smpu_status smpu_tensor_ready(smpu_ctx* ctx, int tensor, void* stream);
+
 /* Bucket-wise micro-batch, for overlap with a still-running backward: micro_begin, then
  * exactly one accumulate_bucket per bucket in any order (buckets are all-reduced in canonical bucket
  * order on every rank).  bucket_grads: host or device fp16 of bucket b only

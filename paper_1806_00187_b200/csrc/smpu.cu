@@ -55,6 +55,10 @@ struct smpu_ctx {
     int world = 1, rank = 0, dev = 0;
     int64_t n = 0;
     std::vector<int64_t> bbegin;   // bucket element offsets, size nb+1
+    std::vector<int> tensor_bucket;                 // bucket of each tensor (plan order)
+    std::vector<int> bucket_tensors;                // tensors per bucket
+    std::vector<int> bucket_tensors_left;           // of the open micro-batch (smpu_tensor_ready)
+    std::vector<char> tensor_seen;                  // of the open micro-batch
     int nb = 0;
 
     float *theta = nullptr, *m = nullptr, *v = nullptr;
@@ -665,6 +669,20 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         return s;
     }
     ctx->nb = (int)ctx->bbegin.size() - 1;
+    {
+        ctx->tensor_bucket.resize(n_tensors);
+        ctx->bucket_tensors.assign(ctx->nb, 0);
+        int64_t off = 0;
+        int b = 0;
+        for (int j = 0; j < n_tensors; ++j) {
+            while (b + 1 < ctx->nb && off >= ctx->bbegin[b + 1]) ++b;
+            ctx->tensor_bucket[j] = b;
+            ctx->bucket_tensors[b]++;
+            off += numel[j];
+        }
+        ctx->bucket_tensors_left = ctx->bucket_tensors;
+        ctx->tensor_seen.assign(n_tensors, 0);
+    }
     ctx->n = ctx->bbegin.back();
     const int64_t n = ctx->n;
 
@@ -935,6 +953,23 @@ smpu_status smpu_micro_begin(smpu_ctx* ctx, int64_t ntokens) {
     ctx->bucket_micro = true;
     ctx->buckets_left = ctx->nb;
     std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    ctx->bucket_tensors_left = ctx->bucket_tensors;
+    std::fill(ctx->tensor_seen.begin(), ctx->tensor_seen.end(), 0);
+    return SMPU_OK;
+}
+
+smpu_status smpu_tensor_ready(smpu_ctx* ctx, int tensor, void* stream) {
+    LIVE(ctx);
+    if (!ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_tensor_ready without smpu_micro_begin");
+    if (tensor < 0 || tensor >= (int)ctx->tensor_bucket.size())
+        return set_err(SMPU_EINVAL, "tensor %d out of [0, %d)", tensor, (int)ctx->tensor_bucket.size());
+    if (ctx->tensor_seen[tensor]) return set_err(SMPU_ESTATE, "tensor %d already ready in this micro-batch", tensor);
+    const int b = ctx->tensor_bucket[tensor];
+    if (ctx->bucket_done[b]) return set_err(SMPU_ESTATE, "bucket %d of tensor %d was already given", b, tensor);
+    ctx->tensor_seen[tensor] = 1;
+    // "when the gradient computation for a layer finishes, we add the result to a synchronization buffer; as
+    // soon as the size of the buffer reaches a predefined threshold we synchronize"
+    if (--ctx->bucket_tensors_left[b] == 0) return smpu_accumulate_bucket(ctx, b, nullptr, stream);
     return SMPU_OK;
 }
 

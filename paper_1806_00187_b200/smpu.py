@@ -54,7 +54,7 @@ class StepResult(ctypes.Structure):
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
            "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets",
            "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate", "smpu_accumulate_many", "smpu_micro_begin",
-           "smpu_accumulate_bucket", "smpu_step", "smpu_allreduce_accumulator", "smpu_graph_capture",
+           "smpu_accumulate_bucket", "smpu_tensor_ready", "smpu_step", "smpu_allreduce_accumulator", "smpu_graph_capture",
            "smpu_graph_launch", "smpu_result", "smpu_get_master", "smpu_get_state", "smpu_set_state",
            "smpu_set_timing", "smpu_kernel_stats", "smpu_kernel_trace", "smpu_last_error", "smpu_destroy"]
 
@@ -87,6 +87,7 @@ def lib():
             "smpu_micro_begin": ([p, i64], st),
             "smpu_accumulate_many": ([p, p, p, i32, p], st),
             "smpu_accumulate_bucket": ([p, i32, p, p], st),
+            "smpu_tensor_ready": ([p, i32, p], st),
             "smpu_step": ([p, p, P(StepResult)], st),
             "smpu_result": ([p, i64, P(StepResult)], st),
             "smpu_allreduce_accumulator": ([p, p], st),
@@ -201,6 +202,9 @@ class UpdateStep:
 
     def accumulate_bucket(self, bucket: int, bucket_grads, stream=None):
         _check(lib().smpu_accumulate_bucket(self._ctx, bucket, _ptr(bucket_grads), _stream(stream)))
+
+    def tensor_ready(self, tensor: int, stream=None):
+        _check(lib().smpu_tensor_ready(self._ctx, tensor, _stream(stream)))
 
     def step(self, stream=None, wait: bool = True):
         """wait=True: returns the result dict; wait=False: asynchronous, returns None."""

@@ -432,3 +432,37 @@ def test_real_training_loop_example(P):
     assert losses[0] > 3.5                      # ~ ln 64 = 4.16 at init
     assert np.mean(losses[-10:]) < 1.5         # learned (noise floor ~0.1*ln 64 + entropy terms)
     assert all(-5 <= s <= 24 for s in scales)
+
+
+def test_tensor_ready_hooks(P):
+    """Per-tensor ready hooks: an in-place producer finishing tensors in a random order; buckets are
+    handed over as their last tensor arrives; same bits as the library-accumulated path; misuse is ESTATE."""
+    import torch
+    tensors = [(f"t{j}", 5_000 + 997 * j, j % 3) for j in range(9)]
+    wl = models.Workload("hooks", tensors, 1, 2)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    x = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=20_000))
+    assert x.n_buckets > 2
+    acc = torch.as_tensor(_DevView(x.accumulator_ptr(), lay.n), device="cuda")
+    rng = np.random.default_rng(7)
+    for u in range(1, 4):
+        grads = [h2t(synth.micro_grad_cpu(wl, lay, u, 0, k, 7)).view(torch.float16) for k in (1, 2)]
+        toks = [1000 + u, 2000 + u]
+        for k in range(2):
+            a.accumulate(grads[k].view(torch.int16), toks[k])
+            x.micro_begin(toks[k])
+            for j in rng.permutation(len(tensors)):
+                lo, hi = lay.begin[j], lay.begin[j + 1]
+                acc[lo:hi].copy_(grads[k][lo:hi]) if k == 0 else acc[lo:hi].add_(grads[k][lo:hi])
+                x.tensor_ready(int(j))
+        ra, rx = a.step(), x.step()
+        assert decisions(ra) == decisions(rx)
+        for w in (0, 1, 2, 3, 4):
+            assert np.array_equal(a.get_state(w), x.get_state(w)), (u, w)
+    x.micro_begin(10)
+    x.tensor_ready(0)
+    with pytest.raises(P.SmpuError) as ei:
+        x.tensor_ready(0)
+    assert ei.value.status == P.smpu.ESTATE
