@@ -121,14 +121,28 @@ __global__ void __launch_bounds__(256) k_ar_lsa(ncclDevComm dc, ncclWindow_t win
     lsa_sync(dc);   // every shard of every rank has been written
 }
 
+// Multicast store of 32 bytes through NVSwitch (NVLS): one store reaches the same offset of every rank's window.
+// (multimem.st moves at most 128 bits: two stores)
+__device__ __forceinline__ void st256_multicast(void* mc, const V8& v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(v.w[0]), "r"(v.w[1]),
+                 "r"(v.w[2]), "r"(v.w[3])
+                 : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.v4.f16x2 [%0], {%1,%2,%3,%4};" ::"l"((char*)mc + 16), "r"(v.w[4]),
+                 "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+
 // Variant with 32-byte units (256-bit peer loads/stores), one unit per thread per iteration: fewer, wider NVLink
 // transactions.  Shards are split on 16-element units; head/tail on rank 0 as above.
-template <int W>
+// MC: the all-gather is one multicast store per unit instead of W peer stores (same bits: the sum is computed
+// once, by the shard's owner, in ascending rank order, as before).
+template <int W, bool MC = false>
 __global__ void __launch_bounds__(256) k_ar_lsa32(ncclDevComm dc, ncclWindow_t win, int64_t lo, int64_t hi) {
     lsa_sync(dc);
     uint16_t* base[W];
 #pragma unroll
     for (int p = 0; p < W; ++p) base[p] = (uint16_t*)ncclGetLsaPointer(win, 0, p);
+    uint16_t* mc = MC ? (uint16_t*)ncclGetLsaMultimemPointer(win, 0, dc) : nullptr;
     const int me = dc.lsaRank;
     const int64_t v0 = (lo + 15) & ~(int64_t)15, v1 = hi & ~(int64_t)15;
     const int64_t units = v1 > v0 ? (v1 - v0) / 16 : 0;
@@ -147,8 +161,12 @@ __global__ void __launch_bounds__(256) k_ar_lsa32(ncclDevComm dc, ncclWindow_t w
         for (int p = 1; p < W; ++p)
 #pragma unroll
             for (int j = 0; j < 8; ++j) a[0].w[j] = hadd2_rn(a[0].w[j], a[p].w[j]);
+        if (MC) {
+            st256_multicast(mc + i0, a[0]);
+        } else {
 #pragma unroll
-        for (int p = 0; p < W; ++p) st256_peer(base[p] + i0, a[0]);
+            for (int p = 0; p < W; ++p) st256_peer(base[p] + i0, a[0]);
+        }
     }
     if (me == 0) {
         auto elem = [&](int64_t i) {

@@ -83,6 +83,7 @@ struct smpu_ctx {
     bool have_devcomm = false;
     int grid_ar = 0;
     bool ar_vec32 = false;                                  // 256-bit peer accesses in the fused all-reduce
+    bool ar_mcast = false;                                  // all-gather by NVLS multicast stores
     size_t dec_area_off = 0;
     bool sharded = false;                                   // SURVEY f2 variant (smpu_config.sharded)
     size_t w16_off = 0;                                     // w16 inside the symmetric window
@@ -378,6 +379,20 @@ smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
             default: return set_err(SMPU_EINVAL, "fused reduce-scatter supports 2..8 ranks");
         }
         CKL("k_rs_lsa");
+        return SMPU_OK;
+    }
+    if (ctx->ar_vec32 && ctx->ar_mcast) {
+        switch (ctx->world) {
+            case 2: k_ar_lsa32<2, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 3: k_ar_lsa32<3, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 4: k_ar_lsa32<4, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 5: k_ar_lsa32<5, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 6: k_ar_lsa32<6, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 7: k_ar_lsa32<7, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 8: k_ar_lsa32<8, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
+        }
+        CKL("k_ar_lsa32<mc>");
         return SMPU_OK;
     }
     if (ctx->ar_vec32) {
@@ -839,8 +854,17 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                 memset(&reqs, 0, sizeof reqs);
                 // one per all-reduce CTA + early decision + late decision + end-of-update (sharded)
                 reqs.lsaBarrierCount = ctx->grid_ar + 3;
+                const char* mcv = getenv("SMPU_AR_MCAST");
+                reqs.lsaMultimem = mcv && atoi(mcv) != 0;
                 r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
-                if (r == ncclSuccess) ctx->have_devcomm = true;
+                if (r != ncclSuccess && reqs.lsaMultimem) {      // no NVLS: fall back to unicast stores
+                    reqs.lsaMultimem = false;
+                    r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
+                }
+                if (r == ncclSuccess) {
+                    ctx->have_devcomm = true;
+                    ctx->ar_mcast = reqs.lsaMultimem;
+                }
             }
             if (r == ncclSuccess && ctx->devcomm.lsaSize == world && ctx->devcomm.lsaRank == rank)
                 ctx->ar_impl = SMPU_AR_FUSED;
