@@ -136,8 +136,8 @@ __device__ __forceinline__ void st256_multicast(void* mc, const V8& v) {
 // transactions.  Shards are split on 16-element units; head/tail on rank 0 as above.
 // MC: the all-gather is one multicast store per unit instead of W peer stores (same bits: the sum is computed
 // once, by the shard's owner, in ascending rank order, as before).
-template <int W, bool MC = false>
-__global__ void __launch_bounds__(256) k_ar_lsa32(ncclDevComm dc, ncclWindow_t win, int64_t lo, int64_t hi) {
+template <int W, bool MC = false, int U = 1>
+__global__ void __launch_bounds__(512) k_ar_lsa32(ncclDevComm dc, ncclWindow_t win, int64_t lo, int64_t hi) {
     lsa_sync(dc);
     uint16_t* base[W];
 #pragma unroll
@@ -152,20 +152,28 @@ __global__ void __launch_bounds__(256) k_ar_lsa32(ncclDevComm dc, ncclWindow_t w
     if (u_hi > units) u_hi = units;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t u = u_lo + tid; u < u_hi; u += nthr) {
-        const int64_t i0 = v0 + u * 16;
-        V8 a[W];
+    for (int64_t u = u_lo + tid; u < u_hi; u += U * nthr) {
+        V8 a[U][W];
 #pragma unroll
-        for (int p = 0; p < W; ++p) a[p] = ld256_peer(base[p] + i0);
+        for (int q = 0; q < U; ++q)
+            if (u + q * nthr < u_hi) {
 #pragma unroll
-        for (int p = 1; p < W; ++p)
+                for (int p = 0; p < W; ++p) a[q][p] = ld256_peer(base[p] + v0 + (u + q * nthr) * 16);
+            }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a[0].w[j] = hadd2_rn(a[0].w[j], a[p].w[j]);
-        if (MC) {
-            st256_multicast(mc + i0, a[0]);
-        } else {
+        for (int q = 0; q < U; ++q) {
+            if (u + q * nthr >= u_hi) break;
+            const int64_t i0 = v0 + (u + q * nthr) * 16;
 #pragma unroll
-            for (int p = 0; p < W; ++p) st256_peer(base[p] + i0, a[0]);
+            for (int p = 1; p < W; ++p)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a[q][0].w[j] = hadd2_rn(a[q][0].w[j], a[q][p].w[j]);
+            if (MC) {
+                st256_multicast(mc + i0, a[q][0]);
+            } else {
+#pragma unroll
+                for (int p = 0; p < W; ++p) st256_peer(base[p] + i0, a[q][0]);
+            }
         }
     }
     if (me == 0) {

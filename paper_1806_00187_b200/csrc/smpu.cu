@@ -84,6 +84,7 @@ struct smpu_ctx {
     int grid_ar = 0;
     bool ar_vec32 = false;                                  // 256-bit peer accesses in the fused all-reduce
     bool ar_mcast = false;                                  // all-gather by NVLS multicast stores
+    int ar_unroll = 1, ar_threads = 256;                    // fused all-reduce shape (tuning knobs)
     size_t dec_area_off = 0;
     bool sharded = false;                                   // SURVEY f2 variant (smpu_config.sharded)
     size_t w16_off = 0;                                     // w16 inside the symmetric window
@@ -395,15 +396,31 @@ smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
         CKL("k_ar_lsa32<mc>");
         return SMPU_OK;
     }
-    if (ctx->ar_vec32) {
+    if (ctx->ar_vec32 && ctx->ar_unroll == 2) {
+        const int t = ctx->ar_threads;
         switch (ctx->world) {
-            case 2: k_ar_lsa32<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 3: k_ar_lsa32<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 4: k_ar_lsa32<4><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 5: k_ar_lsa32<5><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 6: k_ar_lsa32<6><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 7: k_ar_lsa32<7><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 8: k_ar_lsa32<8><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 2: k_ar_lsa32<2, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 3: k_ar_lsa32<3, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 4: k_ar_lsa32<4, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 5: k_ar_lsa32<5, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 6: k_ar_lsa32<6, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 7: k_ar_lsa32<7, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 8: k_ar_lsa32<8, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
+        }
+        CKL("k_ar_lsa32<u2>");
+        return SMPU_OK;
+    }
+    if (ctx->ar_vec32) {
+        const int t = ctx->ar_threads;
+        switch (ctx->world) {
+            case 2: k_ar_lsa32<2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 3: k_ar_lsa32<3><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 4: k_ar_lsa32<4><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 5: k_ar_lsa32<5><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 6: k_ar_lsa32<6><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 7: k_ar_lsa32<7><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
+            case 8: k_ar_lsa32<8><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
             default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
         }
         CKL("k_ar_lsa32");
@@ -843,6 +860,10 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                 ctx->grid_ar = ea && atoi(ea) > 0 ? atoi(ea) : prop.multiProcessorCount;
                 const char* vv = getenv("SMPU_AR_VEC32");
                 ctx->ar_vec32 = vv ? atoi(vv) != 0 : true;
+                const char* uv = getenv("SMPU_AR_UNROLL");
+                ctx->ar_unroll = uv && atoi(uv) == 2 ? 2 : 1;
+                const char* tv = getenv("SMPU_AR_THREADS");
+                ctx->ar_threads = tv && atoi(tv) == 512 ? 512 : 256;
             }
             r = cudaMemset((char*)ctx->acc + ctx->dec_area_off, 0, win_bytes - ctx->dec_area_off) == cudaSuccess
                     ? ncclSuccess
