@@ -39,9 +39,12 @@ def parse():
     ap.add_argument("--update-freq", type=int, default=None)
     ap.add_argument("--bucket-mib", type=float, default=150.0)
     ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
-    ap.add_argument("--sharded", action="store_true",
-                    help="SURVEY f2 variant: reduce-scatter + Adam on 1/W + all-gather of w16 (not the paper's "
-                         "replicated update; bitwise equal to it, tests/test_gpu_multi.py)")
+    ap.add_argument("--optimizer", choices=["auto", "sharded", "replicated"], default="auto",
+                    help="W > 1 update layout. sharded = SURVEY f2: reduce-scatter + Adam on 1/W + all-gather of "
+                         "w16 (bitwise equal to the paper's replicated update, tests/test_gpu_multi.py); "
+                         "replicated = every rank updates the whole vector (the paper's layout); auto = sharded "
+                         "when the fused all-reduce is available, else replicated")
+    ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the call-by-call path (c x smpu_accumulate + smpu_step) instead of the captured "
                          "CUDA graph of the same update (smpu_graph_capture / smpu_graph_launch)")
@@ -391,13 +394,31 @@ def main_ours(args):
         synth.micro_grad_gpu(g, wl, lay, 1, rank, k, 7)
         grads.append(g)
     toks = [synth.ntokens(wl, 1, rank, k) for k in range(1, c + 1)]
+    want_shard = world > 1 and args.allreduce != "nccl" and (args.optimizer == "sharded" or args.sharded or
+                                                             args.optimizer == "auto")
     cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)),
-                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce],
-                           sharded=int(args.sharded and world > 1))
+                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce], sharded=int(want_shard))
     # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
     cfg.growth_interval = 1 << 40
     torch.cuda.synchronize()
-    step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
+    try:
+        step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
+    except P.SmpuError as ex:
+        # auto: the sharded layout needs the fused all-reduce (an LSA window over NVLink); without it every
+        # rank refuses the same way, and all fall back to the paper's replicated update together
+        if not (want_shard and args.optimizer == "auto" and not args.sharded and ex.status == P.smpu.EINVAL):
+            raise
+        print(f"[bench] sharded optimizer unavailable ({ex}); replicated update", file=sys.stderr, flush=True)
+        want_shard = False
+        cfg.sharded = 0
+        if rank == 0:
+            nccl_id = P.unique_id()
+        if world > 1:
+            obj = [nccl_id]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+        step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
+    args.sharded = want_shard
     ar_impl = step.allreduce_impl
     stream = torch.cuda.current_stream()
     if args.mode == "m2":

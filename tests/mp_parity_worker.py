@@ -35,7 +35,8 @@ def main():
     updates = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     impl = sys.argv[3] if len(sys.argv) > 3 else "auto"
     use_graph = len(sys.argv) > 4 and sys.argv[4] == "graph"
-    sharded = len(sys.argv) > 4 and sys.argv[4] == "sharded"
+    sharded = len(sys.argv) > 4 and sys.argv[4] in ("sharded", "sharded_graph")
+    shard_graph = len(sys.argv) > 4 and sys.argv[4] == "sharded_graph"   # the launch bench.py times at W > 1
     many = len(sys.argv) > 4 and sys.argv[4] == "many"
     external = len(sys.argv) > 4 and sys.argv[4] == "external"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -78,6 +79,9 @@ def main():
             for l, h in rr:
                 mark[l:h] += 1
         assert (mark == 1).all(), "shards must partition the vector"
+        if shard_graph:
+            sgbufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)]
+            shard_step.graph_capture(sgbufs)
     orc = O.Oracle(theta0) if rank == 0 else None
     mags = Magnitudes(theta0) if rank == 0 else None
     e = 7
@@ -117,9 +121,15 @@ def main():
                 step.accumulate(h2t(mine[k]), toks[k])
             res = step.step()
         if shard_step is not None:
-            for k in range(c):
-                shard_step.accumulate(h2t(mine[k]), toks[k])
-            rs = shard_step.step()
+            if shard_graph:
+                for k in range(c):
+                    sgbufs[k].copy_(torch.from_numpy(mine[k].view(np.int16)))
+                shard_step.graph_launch(toks)
+                rs = shard_step.result(u)
+            else:
+                for k in range(c):
+                    shard_step.accumulate(h2t(mine[k]), toks[k])
+                rs = shard_step.step()
             if decisions(rs) != decisions(res):
                 failures.append(f"update {u}: sharded decisions {decisions(rs)} vs replicated {decisions(res)}")
             if not np.array_equal(shard_step.get_state(P.smpu.STATE_W16), step.get_state(P.smpu.STATE_W16)):
@@ -181,7 +191,7 @@ def main():
     if rank == 0:
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
               f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
-              f"{' + sharded optimizer bitwise' if sharded else ''}{' via accumulate_many' if many else ''}"
+              f"{' + sharded optimizer bitwise' if sharded else ''}{' (sharded ctx as CUDA graph)' if shard_graph else ''}{' via accumulate_many' if many else ''}"
               f"{' with in-place producer accumulation' if external else ''}")
 
 

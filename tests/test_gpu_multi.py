@@ -18,7 +18,7 @@ def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded
          external=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
-           str(updates), impl] + (["graph"] if graph else []) + (["sharded"] if sharded else []) + \
+           str(updates), impl] + (["graph"] if graph else []) + ([sharded if isinstance(sharded, str) else "sharded"] if sharded else []) + \
           (["many"] if many else []) + (["external"] if external else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
@@ -62,6 +62,15 @@ def test_sharded_optimizer_bitwise_equals_replicated(world):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     _run(world, "real", port=29545 + world, impl="fused", sharded=True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_optimizer_cuda_graph(world):
+    """The launch bench.py times at W > 1: the sharded ctx as one captured CUDA graph per update (device-side
+    decision parity, token counts through the pinned ring) agrees bitwise with the replicated call path."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    _run(world, "real", port=29555 + world, impl="fused", sharded="sharded_graph")
 
 
 @pytest.mark.parametrize("impl", ["nccl", "fused"])

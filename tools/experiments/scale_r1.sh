@@ -1,7 +1,7 @@
 mkdir -p gpurun_out/scale
 python bench.py --steps 20 --warmup 5 --cpu-seconds 5 > gpurun_out/scale/n1.json 2>gpurun_out/scale/n1.err; tail -1 gpurun_out/scale/n1.json | cut -c1-200
 for N in 2 4; do
-for V in "" "--sharded"; do
+for V in "--optimizer replicated" "--optimizer sharded"; do
 tag=n${N}${V:+_sharded}
 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2960$N bench.py --gpus $N --steps 20 --warmup 5 $V > gpurun_out/scale/$tag.log 2>&1
 tail -1 gpurun_out/scale/$tag.log > gpurun_out/scale/$tag.json
