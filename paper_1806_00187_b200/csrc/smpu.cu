@@ -7,13 +7,14 @@
 //   flag int32, stat u32, xs int64[2], DevState, Scalars, loss scale fp32   (device scalars; K0 owns them)
 //   result ring: 64 smpu_step_result in mapped pinned host memory (written by K0).
 //
-// Streams (W > 1): K1 runs on the caller's stream; each bucket's NCCL all-reduce runs on a high-priority
-// comm stream gated by that bucket's ready event (the paper's "background thread", becomes a stream:
-// enqueue is already asynchronous); once the last micro-batch is accumulated, a decision stream all-reduces
-// 16 bytes (N and sum_r max|A_r|) on a second communicator and K0 EARLY decides overflow exactly in the
-// common case; a K2 stream then runs Adam on bucket b as soon as bucket b's all-reduce lands, overlapping
-// the remaining all-reduces.  smpu_step enqueues only the (normally empty) fallback.  W = 1: K1 -> K0 -> K2 on
-// the caller's streams.  No host synchronisation anywhere on the update path.
+// Streams (W > 1): K1 runs on the caller's stream; each bucket's all-reduce (the fused peer-memory kernel of
+// lsa_allreduce.cuh, or NCCL) runs on a high-priority comm stream gated by that bucket's ready event (the
+// paper's "background thread", becomes a stream: enqueue is already asynchronous); once the last
+// micro-batch is accumulated, a decision stream exchanges 16 bytes per rank (N_r and max|A_r|: through peer
+// memory in one kernel, or an NCCL all-reduce on a second communicator) and K0 EARLY decides overflow exactly
+// in the common case; a K2 stream then runs Adam on bucket b as soon as bucket b's all-reduce lands,
+// overlapping the remaining all-reduces.  smpu_step enqueues only the (normally empty) fallback.  W = 1:
+// K1 -> K0 -> K2 on the caller's streams.  No host synchronisation anywhere on the update path.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -132,6 +133,7 @@ struct smpu_ctx {
     };
     std::vector<TraceRec> trace;
     int64_t launches[SMPU_N_KERNELS] = {};
+    int64_t graph_launches[SMPU_N_KERNELS] = {};   // kernels per replay of the captured update, by kind
 };
 
 namespace {
@@ -165,6 +167,20 @@ smpu_status fail_nccl(smpu_ctx* c, ncclResult_t e, const char* what, int line) {
         if (!(ctx)) return set_err(SMPU_EINVAL, "null ctx");                                  \
         if ((ctx)->poisoned) return set_err(SMPU_EPOISONED, "ctx poisoned by an earlier error"); \
     } while (0)
+
+// The peer-memory kernels are templated on the world size W so that their per-rank loops unroll; dispatch a
+// launch macro CALL(W) on the runtime world size.
+#define SMPU_BY_WORLD(world_, CALL, what)                                 \
+    switch (world_) {                                                     \
+        case 2: CALL(2); break;                                           \
+        case 3: CALL(3); break;                                           \
+        case 4: CALL(4); break;                                           \
+        case 5: CALL(5); break;                                           \
+        case 6: CALL(6); break;                                           \
+        case 7: CALL(7); break;                                           \
+        case 8: CALL(8); break;                                           \
+        default: return set_err(SMPU_EINVAL, what " supports 2..8 ranks"); \
+    }
 
 PtrKind classify(const void* p) {
     cudaPointerAttributes a;
@@ -292,22 +308,15 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
 // Adam on this rank's shard ranges of bucket b (sharded variant); one-shot grid, or a small persistent grid for
 // the (normally empty) late fallback
 smpu_status launch_k2_shard(smpu_ctx* ctx, int b, int32_t need, cudaStream_t s) {
+    int launched = 0;   // the caller's Timed counts one launch; rank 0 may add its unaligned head / tail
     for (auto& rg : ctx->shard[b]) {
         if (rg.second <= rg.first) continue;
+        if (launched++) ctx->launches[SMPU_K2]++;
         int grid = grid_for((rg.second - rg.first + 7) / 8, need == DEC_APPLY_LATE ? ctx->grid_k1s : 0x7fffffff);
 #define SMPU_K2S(WW)                                                                                            \
     k2_adam_shard<WW><<<grid, 256, 0, s>>>(ctx->win, ctx->w16_off, ctx->theta, ctx->m, ctx->v, ctx->acc, rg.first, \
                                            rg.second, ctx->sc, need)
-        switch (ctx->world) {
-            case 2: SMPU_K2S(2); break;
-            case 3: SMPU_K2S(3); break;
-            case 4: SMPU_K2S(4); break;
-            case 5: SMPU_K2S(5); break;
-            case 6: SMPU_K2S(6); break;
-            case 7: SMPU_K2S(7); break;
-            case 8: SMPU_K2S(8); break;
-            default: return set_err(SMPU_EINVAL, "sharded Adam supports 2..8 ranks");
-        }
+        SMPU_BY_WORLD(ctx->world, SMPU_K2S, "sharded Adam")
 #undef SMPU_K2S
         CKL("k2_adam_shard");
     }
@@ -367,76 +376,31 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
 }
 
 smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t cs) {
-    const int g = ctx->grid_ar;
+    const int g = ctx->grid_ar, t = ctx->ar_threads;
+    const ncclDevComm& dc = ctx->devcomm;
+    ncclWindow_t win = ctx->win;
+#define SMPU_RS(WW) k_rs_lsa<WW><<<g, 256, 0, cs>>>(dc, win, lo, hi)
+#define SMPU_MC(WW) k_ar_lsa32<WW, true><<<g, 256, 0, cs>>>(dc, win, lo, hi)
+#define SMPU_U2(WW) k_ar_lsa32<WW, false, 2><<<g, t, 0, cs>>>(dc, win, lo, hi)
+#define SMPU_V32(WW) k_ar_lsa32<WW><<<g, t, 0, cs>>>(dc, win, lo, hi)
+#define SMPU_V16(WW) k_ar_lsa<WW><<<g, 256, 0, cs>>>(dc, win, lo, hi)
     if (ctx->sharded) {
-        switch (ctx->world) {
-            case 2: k_rs_lsa<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 3: k_rs_lsa<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 4: k_rs_lsa<4><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 5: k_rs_lsa<5><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 6: k_rs_lsa<6><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 7: k_rs_lsa<7><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 8: k_rs_lsa<8><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            default: return set_err(SMPU_EINVAL, "fused reduce-scatter supports 2..8 ranks");
-        }
-        CKL("k_rs_lsa");
-        return SMPU_OK;
+        SMPU_BY_WORLD(ctx->world, SMPU_RS, "fused reduce-scatter")
+    } else if (ctx->ar_vec32 && ctx->ar_mcast) {
+        SMPU_BY_WORLD(ctx->world, SMPU_MC, "fused all-reduce")
+    } else if (ctx->ar_vec32 && ctx->ar_unroll == 2) {
+        SMPU_BY_WORLD(ctx->world, SMPU_U2, "fused all-reduce")
+    } else if (ctx->ar_vec32) {
+        SMPU_BY_WORLD(ctx->world, SMPU_V32, "fused all-reduce")
+    } else {
+        SMPU_BY_WORLD(ctx->world, SMPU_V16, "fused all-reduce")
     }
-    if (ctx->ar_vec32 && ctx->ar_mcast) {
-        switch (ctx->world) {
-            case 2: k_ar_lsa32<2, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 3: k_ar_lsa32<3, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 4: k_ar_lsa32<4, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 5: k_ar_lsa32<5, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 6: k_ar_lsa32<6, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 7: k_ar_lsa32<7, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 8: k_ar_lsa32<8, true><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
-        }
-        CKL("k_ar_lsa32<mc>");
-        return SMPU_OK;
-    }
-    if (ctx->ar_vec32 && ctx->ar_unroll == 2) {
-        const int t = ctx->ar_threads;
-        switch (ctx->world) {
-            case 2: k_ar_lsa32<2, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 3: k_ar_lsa32<3, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 4: k_ar_lsa32<4, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 5: k_ar_lsa32<5, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 6: k_ar_lsa32<6, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 7: k_ar_lsa32<7, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 8: k_ar_lsa32<8, false, 2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
-        }
-        CKL("k_ar_lsa32<u2>");
-        return SMPU_OK;
-    }
-    if (ctx->ar_vec32) {
-        const int t = ctx->ar_threads;
-        switch (ctx->world) {
-            case 2: k_ar_lsa32<2><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 3: k_ar_lsa32<3><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 4: k_ar_lsa32<4><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 5: k_ar_lsa32<5><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 6: k_ar_lsa32<6><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 7: k_ar_lsa32<7><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            case 8: k_ar_lsa32<8><<<g, t, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-            default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
-        }
-        CKL("k_ar_lsa32");
-        return SMPU_OK;
-    }
-    switch (ctx->world) {
-        case 2: k_ar_lsa<2><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        case 3: k_ar_lsa<3><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        case 4: k_ar_lsa<4><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        case 5: k_ar_lsa<5><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        case 6: k_ar_lsa<6><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        case 7: k_ar_lsa<7><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        case 8: k_ar_lsa<8><<<g, 256, 0, cs>>>(ctx->devcomm, ctx->win, lo, hi); break;
-        default: return set_err(SMPU_EINVAL, "fused all-reduce supports 2..8 ranks");
-    }
-    CKL("k_ar_lsa");
+#undef SMPU_RS
+#undef SMPU_MC
+#undef SMPU_U2
+#undef SMPU_V32
+#undef SMPU_V16
+    CKL(ctx->sharded ? "k_rs_lsa" : "k_ar_lsa");
     return SMPU_OK;
 }
 
@@ -488,8 +452,9 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
 }
 
 // W > 1, once every bucket of the last micro-batch is accumulated: the exact early overflow decision
-// (k0_early) from one 16-byte all-reduce on a second communicator, then Adam per bucket on its own stream,
-// each bucket right behind its gradient all-reduce -- K2 overlaps the remaining all-reduces.
+// (k0_early_lsa through peer memory, or k0_early after a 16-byte NCCL all-reduce on a second communicator),
+// then Adam per bucket on its own stream, each bucket right behind its gradient all-reduce -- K2 overlaps the
+// remaining all-reduces.
 // token count source of the decision kernels: kernel argument, or tok_dev inside a captured graph
 const int64_t* tok_src(const smpu_ctx* ctx) { return ctx->capturing ? ctx->tok_dev : nullptr; }
 
@@ -498,16 +463,7 @@ smpu_status launch_decision_lsa(smpu_ctx* ctx, cudaStream_t ds) {
     k0_early_lsa<WW><<<1, 32, 0, ds>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->stat,                     \
                                        ctx->local_tokens, tok_src(ctx), ctx->xs, ctx->st, ctx->sc, ctx->scale,   \
                                        ctx->ring_dev, kRing - 1, ctx->dcfg, (uint32_t)ctx->grid_ar)
-    switch (ctx->world) {
-        case 2: SMPU_DEC(2); break;
-        case 3: SMPU_DEC(3); break;
-        case 4: SMPU_DEC(4); break;
-        case 5: SMPU_DEC(5); break;
-        case 6: SMPU_DEC(6); break;
-        case 7: SMPU_DEC(7); break;
-        case 8: SMPU_DEC(8); break;
-        default: return set_err(SMPU_EINVAL, "fused decision supports 2..8 ranks");
-    }
+    SMPU_BY_WORLD(ctx->world, SMPU_DEC, "fused decision")
 #undef SMPU_DEC
     CKL("k0_early_lsa");
     return SMPU_OK;
@@ -800,12 +756,10 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         IK(cudaEventRecord(ctx->stage_free[j], ctx->copy_stream));
     }
 
-    // persistent grids: resident CTAs per SM x SMs
+    // K1 / K2: one-shot grids by default (grid_cap); the K1s sweep: a persistent grid of resident CTAs x SMs
     int occ = 0;
-    IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_accumulate<false, false>, 256, 0));
     ctx->grid_k1 = grid_cap("SMPU_K1_CTAS_PER_SM", prop.multiProcessorCount, 0);
     ctx->k1_oneshot = ctx->grid_k1 == 0x7fffffff;
-    IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_adam, 256, 0));
     ctx->grid_k2 = grid_cap("SMPU_K2_CTAS_PER_SM", prop.multiProcessorCount, 0);
     ctx->k2_oneshot = ctx->grid_k2 == 0x7fffffff;
     {
@@ -1181,16 +1135,7 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
 #define SMPU_KL(WW)                                                                                           \
     k0_late_lsa<WW><<<1, 32, 0, s>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->flag, ctx->xs, ctx->st,  \
                                      ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg, bi)
-            switch (ctx->world) {
-                case 2: SMPU_KL(2); break;
-                case 3: SMPU_KL(3); break;
-                case 4: SMPU_KL(4); break;
-                case 5: SMPU_KL(5); break;
-                case 6: SMPU_KL(6); break;
-                case 7: SMPU_KL(7); break;
-                case 8: SMPU_KL(8); break;
-                default: return set_err(SMPU_EINVAL, "sharded path supports 2..8 ranks");
-            }
+            SMPU_BY_WORLD(ctx->world, SMPU_KL, "sharded path")
 #undef SMPU_KL
             CKL("k0_late_lsa");
         }
@@ -1284,6 +1229,9 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     const bool timing = ctx->timing;
     ctx->timing = false;
     ctx->capturing = true;
+    // the launch counters tick while the update is captured: the difference is one replay's kernels
+    int64_t before[SMPU_N_KERNELS];
+    memcpy(before, ctx->launches, sizeof before);
     cudaGraph_t graph = nullptr;
     smpu_status st = SMPU_OK;
     cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
@@ -1314,6 +1262,10 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     }
     ctx->capturing = false;
     ctx->timing = timing;
+    for (int k = 0; k < SMPU_N_KERNELS; ++k) {
+        ctx->graph_launches[k] = ctx->launches[k] - before[k];
+        ctx->launches[k] = before[k];
+    }
     ctx->micro = 0;
     ctx->bucket_micro = false;
     ctx->local_tokens = 0;
@@ -1349,16 +1301,7 @@ smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, 
     if (ctx->attempts >= kRing) CK(cudaEventSynchronize(ctx->ring_ev[slot]));   // slot's previous copy has run
     ctx->tok_host[slot] = N;
     CK(cudaMemcpyAsync(ctx->tok_dev, &ctx->tok_host[slot], sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    if (ctx->graph_direct) {
-        ctx->launches[SMPU_K1S] += 1;
-    } else if (ctx->graph_resident) {
-        ctx->launches[SMPU_K1_MANY] += ctx->world > 1 ? ctx->nb : 1;
-    } else {
-        ctx->launches[SMPU_K1_FIRST] += 1;
-        ctx->launches[SMPU_K1_ADD] += ctx->cfg.update_freq - 1;
-    }
-    ctx->launches[SMPU_K0] += 1;
-    ctx->launches[SMPU_K2] += 1;
+    for (int k = 0; k < SMPU_N_KERNELS; ++k) ctx->launches[k] += ctx->graph_launches[k];
     CK(cudaGraphLaunch(ctx->graph_exec, s));
     ctx->attempts++;
     CK(cudaEventRecord(ctx->ring_ev[(ctx->attempts - 1) % kRing], s));

@@ -257,7 +257,10 @@ def test_graph_replay_bitwise_equals_call_path(P):
     b = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
     orc = O.Oracle(theta0)
     bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(3)]
+    a.kernel_stats(reset=True)
+    b.kernel_stats(reset=True)      # drops init's theta -> w16 cast
     b.graph_capture(bufs)
+    assert sum(v["launches"] for v in b.kernel_stats(reset=True).values()) == 0   # capturing launches nothing
     for u in range(1, 7):
         e = orc.e
         grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in (1, 2, 3)]
@@ -272,6 +275,11 @@ def test_graph_replay_bitwise_equals_call_path(P):
         assert decisions(ra) == decisions(rb) == oracle_decisions(ores), u
         for w in (0, 1, 2, 3, 4, 5):
             assert np.array_equal(a.get_state(w), b.get_state(w)), (u, w)
+    # the launch counters (bench.py's gpu_launches) count each replay's kernels like the call path's
+    la = {k: v["launches"] for k, v in a.kernel_stats().items()}
+    lb = {k: v["launches"] for k, v in b.kernel_stats().items()}
+    assert (la["k1_first"], la["k1_add"], la["k0_decide"], la["k2_adam"]) == (6, 12, 6, 6), la
+    assert la == lb, (la, lb)
 
 
 def test_accumulate_many_bitwise_equals_streaming(P):
