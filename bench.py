@@ -45,6 +45,9 @@ def parse():
                          "replicated = every rank updates the whole vector (the paper's layout); auto = sharded "
                          "when the fused all-reduce is available, else replicated")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
+    ap.add_argument("--fuse-final", type=int, choices=[0, 1], default=1,
+                    help="W = 1: fuse the last micro-batch's accumulation into Adam (smpu_config.fuse_final, the "
+                         "library default; 0 = accumulate, decide, then Adam)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the call-by-call path (c x smpu_accumulate + smpu_step) instead of the captured "
                          "CUDA graph of the same update (smpu_graph_capture / smpu_graph_launch)")
@@ -397,7 +400,9 @@ def main_ours(args):
     want_shard = world > 1 and args.allreduce != "nccl" and (args.optimizer == "sharded" or args.sharded or
                                                              args.optimizer == "auto")
     cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)),
-                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce], sharded=int(want_shard))
+                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce], sharded=int(want_shard),
+                           fuse_final=args.fuse_final)
+    fused = world == 1 and args.fuse_final == 1
     # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
     cfg.growth_interval = 1 << 40
     torch.cuda.synchronize()
@@ -528,15 +533,18 @@ def main_ours(args):
         ms_res = _max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
         last = step.result(step.scalars()["attempts"])
         assert last["applied"] == 1 and last["overflow"] == 0, last
-        res_bytes = n * (2 * c + 2 + 28)
+        # one pass over the c gradients (+ the accumulator written, then Adam's 28) or, fused, straight into Adam
+        res_bpe = 2 * c + 26 if fused else 2 * c + 2 + 28
+        res_bytes = n * res_bpe
         graph_info["resident_microbatches"] = {
             "ms_per_step": ms_res, "value": world * c * n / (ms_res * 1e-3), "unit": UNIT,
-            "path_hbm_gbs": res_bytes / (ms_res * 1e-3) / 1e9, "bytes_per_elem": 2 * c + 2 + 28,
+            "path_hbm_gbs": res_bytes / (ms_res * 1e-3) / 1e9, "bytes_per_elem": res_bpe,
             "api": "smpu_graph_capture(..., SMPU_GRAPH_RESIDENT) -> one smpu_accumulate_many over c buffers"}
 
     # ---- exposed communication: the same per-GPU work through a world = 1 ctx on the same GPU
     exposed = None
     if world > 1:
+        cfg.fuse_final = 0     # the world > 1 kernels (accumulate, decide, Adam), minus the exchange
         step1 = P.UpdateStep(wl.numel, theta0, cfg, world=1, rank=0, device=local)
 
         if not args.no_graph:
@@ -600,11 +608,16 @@ def main_ours(args):
     hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
     peak_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "of fallback (B200_PROFILING.md)"
     nb = step.n_buckets
-    # algorithmic bytes per launch: K1 first 4 B/elem, K1 add 6, K1s 2, K2 28
+    # algorithmic bytes per launch: K1 first 4 B/elem, K1 add 6, K1s 2, K2 28, K12 (the
+    # fused last micro-batch + Adam, W = 1) 30 (28 at c = 1: no accumulator read)
     # (K1s only sweeps when the early decision was undecided; with G_real it returns at once)
-    per_elem = {"k1_first": 4, "k1_add": 6, "k2_adam": 28}
-    elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n,
-                      "k2_adam": sum(h - l for l, h in step.shard_ranges())}
+    per_elem = {"k1_first": 4, "k1_add": 6, "k2_adam": 28, "k12_fused": 30 if c > 1 else 28}
+    if fused:
+        elems_per_step = {"k1_first": n if c > 1 else 0, "k1_add": max(c - 2, 0) * n, "k2_adam": 0,
+                          "k12_fused": n}
+    else:
+        elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n, "k2_adam": sum(h - l for l, h in step.shard_ranges()),
+                          "k12_fused": 0}
     kernels = {}
     for k, bpe in per_elem.items():
         st = kstat[k]
@@ -622,14 +635,15 @@ def main_ours(args):
     roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["achieved_gbs"], "peak": hbm_peak,
             "unit": "GB/s", "frac": kernels[dom]["achieved_gbs"] / hbm_peak, "peak_source": peak_src,
             "traffic": traffic, "frac_of_ncu_dram_peak": kernels[dom]["achieved_gbs"] / ncu_dram_peak}
-    path_bytes = n * (6 * c - 2 + 28)
+    path_bytes = n * ((28 if c == 1 else 6 * c + 22) if fused else 6 * c - 2 + 28)
     out = {"metric": METRIC, "value": world * c * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f16+f32", "data": "synthetic",
            "config": {"workload": wl.name, "n_params": n, "n_tensors": len(wl.numel), "update_freq": c,
                       "world": world, "bucket_mib": args.bucket_mib, "n_buckets": nb,
                       "tokens_per_update": int(sum(toks)) * world, "generator": "G_real (SURVEY 8(d.2))",
-                      "parallelism": f"dp{world}",
+                      "parallelism": f"dp{world}", "fuse_final": int(fused),
+                      "path_bytes_per_elem": path_bytes / n,
                       "optimizer": "sharded (SURVEY f2)" if (args.sharded and world > 1) else "replicated (paper)", "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"},
            "update_steps_per_s": 1000.0 / ms,
            "path_hbm_gbs": path_bytes / (ms * 1e-3) / 1e9,

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SMPU_ABI_VERSION 1
+#define SMPU_ABI_VERSION 2
 #define SMPU_NCCL_ID_BYTES 128
 
 typedef struct smpu_ctx smpu_ctx;
@@ -69,6 +69,13 @@ typedef struct {
                                   1: sharded variant (world > 1, fused all-reduce): reduce-scatter,
                                   Adam on this rank's shard only, all-gather of w16.  theta/m/v are then valid
                                   only on smpu_shard_ranges; per element the arithmetic is unchanged.        */
+    int32_t fuse_final;        /* world == 1 (ignored above): 1 (default) fuses the last micro-batch's accumulation
+                                  into Adam -- one pass of 30 B/element instead of K1's 6 + Adam's 28 (28 instead
+                                  of 4 + 28 at c = 1).  The overflow decision needs all of R, so the update is
+                                  computed speculatively into a second copy of theta/m/v (+12 B per parameter)
+                                  that becomes current only if R was finite; on a skip w16 is re-cast from the
+                                  current theta.  Same arithmetic per element, bitwise (tested); R itself is then
+                                  never stored (SMPU_STATE_ACCUM).  0: accumulate, decide, then Adam.            */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */
@@ -98,13 +105,16 @@ enum {
     SMPU_STATE_M = 1,          /* fp32[n] Adam first moment                                               */
     SMPU_STATE_V = 2,          /* fp32[n] Adam second moment                                              */
     SMPU_STATE_W16 = 3,        /* fp16[n] model weights (the re-cast copy)                                */
-    SMPU_STATE_ACCUM = 4,      /* fp16[n] gradient accumulator (after step: the reduced gradient R)       */
+    SMPU_STATE_ACCUM = 4,      /* fp16[n] gradient accumulator: after step, the reduced gradient R; with
+                                  fuse_final at world 1 the sum of the first c - 1 micro-batches instead
+                                  (untouched at c = 1), because R is consumed without being stored        */
     SMPU_STATE_SCALARS = 5     /* int64[4] = {e, clean_streak, num_updates, attempts}                     */
 };
 
 /* kernel ids of smpu_kernel_stats */
 enum { SMPU_K1_FIRST = 0, SMPU_K1_ADD = 1, SMPU_K1S = 2, SMPU_K0 = 3, SMPU_K2 = 4, SMPU_KCAST = 5,
-       SMPU_ALLREDUCE = 6, SMPU_DECISION_AR = 7, SMPU_K1_MANY = 8, SMPU_N_KERNELS = 9 };
+       SMPU_ALLREDUCE = 6, SMPU_DECISION_AR = 7, SMPU_K1_MANY = 8, SMPU_K12 = 9 /* fused last micro + Adam */,
+       SMPU_N_KERNELS = 10 };
 
 /* flags of smpu_graph_capture */
 enum { SMPU_GRAPH_STREAMING = 0, SMPU_GRAPH_RESIDENT = 1 };
@@ -132,7 +142,8 @@ smpu_status smpu_plan_buckets(const int64_t* numel, int n_tensors, int64_t bucke
  *   numel        host int64[n_tensors] > 0, gradient-ready order; copied.
  *   init_params  host or device fp32[n]: theta_0; copied.  Rank 0's copy is broadcast so all replicas
  *                start bitwise identical (P:55-57 synchronous data parallelism).
- * Allocates theta, m, v (fp32), w16, accumulator (fp16) on the device: 16 B per parameter. */
+ * Allocates theta, m, v (fp32), w16, accumulator (fp16) on the device: 16 B per parameter (+12 for the
+ * second theta/m/v of fuse_final at world 1). */
 smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
                       int cuda_device, const int64_t* numel, int n_tensors, const float* init_params);
 
@@ -210,9 +221,9 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out);
  * buffers; their addresses are frozen, their contents are read at replay time) followed by smpu_step into a
  * graph owned by the ctx (replacing any earlier one); flags = SMPU_GRAPH_RESIDENT records one
  * smpu_accumulate_many over all c buffers instead (the producer keeps the c gradients until the replay).
- * It enqueues nothing.  With update_freq = 1 at world = 1 the graph tests the buffer for overflow in place and
- * Adam reads it directly (R = g_1: nothing to copy; the accumulator is then not written by the replays).  At world > 1 it needs the fused
- * all-reduce (EINVAL with SMPU_AR_NCCL).  smpu_graph_launch replays it on
+ * It enqueues nothing.  With fuse_final = 0, update_freq = 1 and world = 1 the graph tests the buffer for
+ * overflow in place and Adam reads it directly (the accumulator is then not written by the replays).  At
+ * world > 1 it needs the fused all-reduce (EINVAL with SMPU_AR_NCCL).  smpu_graph_launch replays it on
  * `stream` with this update's token counts ntokens[0..c) (host): identical arithmetic and decisions to the
  * call-by-call path, one launch instead of c + 2 (or, at world > 1, the bucket all-reduces, decision and
  * per-bucket Adam as well); asynchronous, results via smpu_result.  Both ESTATE inside an update.  Launch

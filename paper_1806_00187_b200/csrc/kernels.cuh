@@ -68,9 +68,9 @@ __device__ __forceinline__ void st128(void* p, const V4& v) {
 
 // Programmatic dependent launch (sm_90+): `pdl_trigger` lets the next kernel of the stream start its CTAs while
 // this one finishes its last wave; `pdl_wait` blocks until the previous kernel has completed and its memory is
-// visible.  Every kernel below waits before its first dependent load or any store; only loads of data no
-// incomplete kernel writes (the caller's micro-gradient, theta/m/v of the previous update) may precede it.
-// Without the launch attribute both are no-ops.
+// visible.  Every kernel below waits before its first dependent load or any store; only loads of the caller's
+// micro-gradient may precede it (its writer is the caller's own kernel, which does not trigger early, so it
+// completed before our chain could start).  Without the launch attribute both are no-ops.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -385,6 +385,7 @@ struct DevState {          // device-resident scaler / optimizer counters
     int64_t clean;         // consecutive clean updates
     int64_t t;             // applied updates
     int64_t attempts;      // update attempts
+    int64_t bank;          // fused final micro-batch (W = 1): which copy of theta/m/v is current (0 / 1)
 };
 
 // decision states (Scalars::state)
@@ -418,6 +419,21 @@ __device__ __forceinline__ float lr_at(int64_t t, const DevCfg& c) {
     return __double2float_rn(__dmul_rn(c.peak_lr, f));
 }
 
+// Adam scalars of applied update t, from the exponent e the gradients carry (before growth) and N.
+__device__ void adam_scalars(int64_t t, int32_t e, int64_t N, float lr, const DevCfg& cfg, Scalars* sc) {
+    double sN = ldexp((double)N, (int)e);
+    double bc1 = 1.0 - pow(cfg.beta1, (double)t);
+    double bc2 = 1.0 - pow(cfg.beta2, (double)t);
+    sc->inv_sN = __double2float_rn(1.0 / sN);
+    sc->step = __double2float_rn((double)lr / bc1);
+    sc->inv_sqrt_bc2 = __double2float_rn(1.0 / sqrt(bc2));
+    sc->b1 = (float)cfg.beta1;
+    sc->omb1 = (float)(1.0 - cfg.beta1);
+    sc->b2 = (float)cfg.beta2;
+    sc->omb2 = (float)(1.0 - cfg.beta2);
+    sc->eps = (float)cfg.eps;
+}
+
 // The scaler step + Adam scalars + result record, once per update attempt.
 // Returns the decision state written (DEC_APPLY / DEC_SKIP; apply_state for a late decision).
 __device__ void decide(int overflow, int64_t N, DevState* st, Scalars* sc, float* loss_scale,
@@ -447,18 +463,7 @@ __device__ void decide(int overflow, int64_t N, DevState* st, Scalars* sc, float
         s.clean += 1;
         r.applied = 1;
         r.lr = lr_at(s.t, cfg);
-        // Adam scalars for this update, from the exponent the gradients carry (before growth)
-        double sN = ldexp((double)N, (int)r.scale_log2_used);
-        double bc1 = 1.0 - pow(cfg.beta1, (double)s.t);
-        double bc2 = 1.0 - pow(cfg.beta2, (double)s.t);
-        sc->inv_sN = __double2float_rn(1.0 / sN);
-        sc->step = __double2float_rn((double)r.lr / bc1);
-        sc->inv_sqrt_bc2 = __double2float_rn(1.0 / sqrt(bc2));
-        sc->b1 = (float)cfg.beta1;
-        sc->omb1 = (float)(1.0 - cfg.beta1);
-        sc->b2 = (float)cfg.beta2;
-        sc->omb2 = (float)(1.0 - cfg.beta2);
-        sc->eps = (float)cfg.eps;
+        adam_scalars(s.t, r.scale_log2_used, N, r.lr, cfg, sc);
         if (s.clean >= cfg.growth) {                   // P:158 "scales the loss up if no overflows ... 2,000"
             s.e = s.e + 1 > cfg.emax ? cfg.emax : s.e + 1;
             s.clean = 0;
@@ -476,9 +481,10 @@ __device__ void decide(int overflow, int64_t N, DevState* st, Scalars* sc, float
 
 // W = 1: the last K1 tested the reduced (= local) gradient exactly.
 // tok_ptr != nullptr (CUDA-graph replays): the token count is read from the device at run time
+// fused: the update ran speculatively (k12_fused wrote the other bank); applying = making that bank current.
 __global__ void k0_decide(int* __restrict__ flag, int64_t tokens, const int64_t* __restrict__ tok_ptr,
                           DevState* __restrict__ st, Scalars* __restrict__ sc, float* __restrict__ loss_scale,
-                          smpu_step_result* __restrict__ ring, int ring_mask, DevCfg cfg) {
+                          smpu_step_result* __restrict__ ring, int ring_mask, DevCfg cfg, int fused = 0) {
     pdl_trigger();
     pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -486,6 +492,22 @@ __global__ void k0_decide(int* __restrict__ flag, int64_t tokens, const int64_t*
     const int overflow = *(volatile int*)flag != 0;
     *(volatile int*)flag = 0;                          // re-armed for the next update
     decide(overflow, tokens, st, sc, loss_scale, ring, ring_mask, cfg, DEC_APPLY);
+    if (fused && sc->state == DEC_APPLY) st->bank ^= 1;
+}
+
+// W = 1 with the fused final micro-batch: before it, the Adam scalars of update t+1 as if it will apply (the
+// same fp64 arithmetic as decide()); N = 0 (discarded) turns k12_fused off.
+__global__ void k0_fused_prep(int64_t tokens, const int64_t* __restrict__ tok_ptr, const DevState* __restrict__ st,
+                              Scalars* __restrict__ sc, DevCfg cfg) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (tok_ptr) tokens = *tok_ptr;
+    const DevState s = *st;
+    if (tokens <= 0) {
+        sc->state = DEC_SKIP;
+        return;
+    }
+    adam_scalars(s.t + 1, (int32_t)s.e, tokens, lr_at(s.t + 1, cfg), cfg, sc);
+    sc->state = DEC_APPLY;
 }
 
 // W > 1, before the gradient all-reduces finish.  xs = {N, sum_r M_r} summed over ranks by one int64
@@ -637,19 +659,14 @@ __global__ void __launch_bounds__(256, 4) k2_adam_1(float* __restrict__ theta, f
     if (vbeg > hi) vbeg = hi;
     const int64_t nvec = (hi - vbeg) / 8, vend = vbeg + nvec * 8;
     pdl_trigger();
-    // theta/m/v were last written by the previous update's Adam, complete before our predecessors could start
-    V8 t0, m0, v0;
-    if (tid < nvec) {
-        const int64_t i0 = vbeg + tid * 8;
-        t0 = ld256(theta + i0);
-        m0 = ld256(m + i0);
-        v0 = ld256(v + i0);
-    }
+    // No load before the wait: with small grids every kernel of the chain triggers its dependent at once, so
+    // the previous update's Adam (the last writer of theta/m/v) may still be running here.
     pdl_wait();
     if (decision_of(scp) != need) return;
     const Scalars s = *scp;
     if (tid < nvec) {
         const int64_t i0 = vbeg + tid * 8;
+        V8 t0 = ld256(theta + i0), m0 = ld256(m + i0), v0 = ld256(v + i0);
         V4 r0 = ld128_ro(R + i0);
         V4 w0;
         adam_unit(r0, t0, m0, v0, w0, s);
@@ -668,6 +685,107 @@ __global__ void __launch_bounds__(256, 4) k2_adam_1(float* __restrict__ theta, f
     };
     for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
     for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+}
+
+// ---------------------------------------------------------------------------------------------- K12
+// W = 1: the last micro-batch's accumulation fused into Adam (30 instead of 6 + 28 bytes per element; 28 at
+// c = 1).  Per element R = [HAS_ACC ? A : g_0] (+ g_k for the rest, in order, fp16 RNE: K1's additions), then
+// exactly K2's arithmetic (adam_unit / adam_elem).  Speculative: the overflow decision needs all of R, so the
+// update is computed from bank b of theta/m/v into bank 1-b and K0 makes it current only if R was finite; w16
+// is written in place and re-cast from the current bank on a skip (kc_restore).  R itself is never stored.
+template <bool HAS_ACC>
+__global__ void __launch_bounds__(256, 4) k12_fused(const uint16_t* __restrict__ acc, ManyPtrs P, int count,
+                                                    int64_t lo, int64_t hi, float* th0, float* m0, float* v0,
+                                                    float* th1, float* m1, float* v1, uint16_t* __restrict__ w16,
+                                                    const DevState* __restrict__ st, const Scalars* __restrict__ scp,
+                                                    int* __restrict__ flag) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 7) & ~(int64_t)7;
+    if (vbeg > hi) vbeg = hi;
+    bool vec_ok = true;
+    for (int k = 0; k < count; ++k) vec_ok &= ((reinterpret_cast<uintptr_t>(P.g[k] + (vbeg - lo)) & 15) == 0);
+    const int64_t nvec = vec_ok ? (hi - vbeg) / 8 : 0, vend = vbeg + nvec * 8;
+    // Issue order matters (the asm loads are volatile, so they stay in program order): the accumulator and the
+    // first gradients do not depend on the decision state or the bank, so they go first and are in flight
+    // while those are read; theta/m/v follow before any add, so one thread never waits for two latencies.
+    const int k0 = HAS_ACC ? 0 : 1;
+    const int64_t i0 = vbeg + tid * 8, r0 = i0 - lo;
+    V4 x, y[4];
+    if (tid < nvec) {
+        x = HAS_ACC ? ld128_ro(acc + i0) : ld128_ro(P.g[0] + r0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (k0 + j < count) y[j] = ld128_ro(P.g[k0 + j] + r0);
+    }
+    if (decision_of(scp) != DEC_APPLY) return;         // N = 0: the update is discarded
+    const Scalars s = *scp;
+    const bool b = st->bank != 0;
+    const float* __restrict__ ti = b ? th1 : th0;
+    const float* __restrict__ mi = b ? m1 : m0;
+    const float* __restrict__ vi = b ? v1 : v0;
+    float* __restrict__ to = b ? th0 : th1;
+    float* __restrict__ mo = b ? m0 : m1;
+    float* __restrict__ vo = b ? v0 : v1;
+    uint32_t bad = 0;
+    if (tid < nvec) {
+        V8 t = ld256_ro(ti + i0), m = ld256_ro(mi + i0), v = ld256_ro(vi + i0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (k0 + j < count) {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) x.w[w] = hadd2_rn(x.w[w], y[j].w[w]);
+            }
+        for (int k = k0 + 4; k < count; k += 4) {     // resident micro-batches beyond the first four
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < count) y[j] = ld128_ro(P.g[k + j] + r0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < count) {
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) x.w[w] = hadd2_rn(x.w[w], y[j].w[w]);
+                }
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) bad |= nonfinite_bits(x.w[w]);
+        V4 w16v;
+        adam_unit(x, t, m, v, w16v, s);
+        st256(to + i0, t);
+        st256(mo + i0, m);
+        st256(vo + i0, v);
+        st128(w16 + i0, w16v);
+    }
+    auto elem = [&](int64_t i) {
+        uint32_t x = HAS_ACC ? (uint32_t)acc[i] : (uint32_t)P.g[0][i - lo];
+        for (int k = HAS_ACC ? 0 : 1; k < count; ++k) x = hadd2_rn(x, (uint32_t)P.g[k][i - lo]) & 0xFFFFu;
+        if (h_nonfinite((uint16_t)x)) bad |= 1u;
+        float th = ti[i], mm = mi[i], vv = vi[i];
+        adam_elem(__half2float(__ushort_as_half((uint16_t)x)), th, mm, vv, s);
+        to[i] = th;
+        mo[i] = mm;
+        vo[i] = vv;
+        w16[i] = __half_as_ushort(__float2half_rn(th));
+    };
+    if (vec_ok) {
+        for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+        for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
+    }
+    raise_flag(bad != 0, flag);
+}
+
+// After a skipped fused update: w16 = rn16(current theta) again (k12_fused wrote it speculatively).  Returns at
+// once unless K0 decided to skip.
+__global__ void __launch_bounds__(256) kc_restore(const float* __restrict__ th0, const float* __restrict__ th1,
+                                                  const DevState* __restrict__ st, const Scalars* __restrict__ scp,
+                                                  uint16_t* __restrict__ w16, int64_t n) {
+    if (decision_of(scp) != DEC_SKIP) return;
+    const float* __restrict__ th = st->bank ? th1 : th0;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr)
+        w16[i] = __half_as_ushort(__float2half_rn(th[i]));
 }
 
 // ---------------------------------------------------------------------------------------------- Kc

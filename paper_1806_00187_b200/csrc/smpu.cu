@@ -2,6 +2,7 @@
 //
 // Layout in HBM (one allocation per array, 16 B per parameter in total):
 //   theta fp32[n], m fp32[n], v fp32[n]       fp32 master weights + Adam moments
+//   theta_b, m_b, v_b fp32[n]                 second bank of them (fuse_final at W = 1: the speculative update)
 //   w16   fp16[n]                             fp16 model weights, re-cast each update
 //   acc   fp16[n]                             accumulator; buckets are views of it
 //   flag int32, stat u32, xs int64[2], DevState, Scalars, loss scale fp32   (device scalars; K0 owns them)
@@ -63,6 +64,9 @@ struct smpu_ctx {
     int nb = 0;
 
     float *theta = nullptr, *m = nullptr, *v = nullptr;
+    float *theta_b = nullptr, *m_b = nullptr, *v_b = nullptr;   // second bank (fuse_final, world 1)
+    bool fused = false;            // fuse_final in effect: the last micro-batch runs k12_fused
+    bool fused_prepped = false;    // k0_fused_prep enqueued for the open update
     uint16_t *w16 = nullptr, *acc = nullptr;
     int* flag = nullptr;
     uint32_t* stat = nullptr;      // local max fp16 magnitude bits of the last micro-batch's output (W > 1)
@@ -343,9 +347,65 @@ smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaS
     return SMPU_OK;
 }
 
-// accumulate src (host or device) into acc[lo, hi)
+// token count source of the decision kernels: kernel argument, or tok_dev inside a captured graph
+const int64_t* tok_src(const smpu_ctx* ctx) { return ctx->capturing ? ctx->tok_dev : nullptr; }
+
+// W = 1, fuse_final: the last micro-batch's elements [lo, hi) fused into Adam (k12_fused).  g[k] points at
+// element lo of micro-gradient k; has_acc: R starts from the accumulator (else from g[0]).  The first call of
+// an update first enqueues the Adam scalars (k0_fused_prep).
+smpu_status launch_k12(smpu_ctx* ctx, const uint16_t* const* g, int count, int64_t lo, int64_t hi, bool has_acc,
+                       cudaStream_t s) {
+    if (!ctx->fused_prepped) {
+        Timed t(ctx, SMPU_K0, s);
+        k0_fused_prep<<<1, 32, 0, s>>>(ctx->local_tokens, tok_src(ctx), ctx->st, ctx->sc, ctx->dcfg);
+        CKL("k0_fused_prep");
+        ctx->fused_prepped = true;
+    }
+    if (hi <= lo) return SMPU_OK;
+    ManyPtrs P;
+    for (int k = 0; k < count; ++k) P.g[k] = g[k];
+    const int grid = grid_for((hi - lo + 7) / 8, 0x7fffffff);
+    Timed t(ctx, SMPU_K12, s);
+    if (has_acc)
+        k12_fused<true><<<grid, 256, 0, s>>>(ctx->acc, P, count, lo, hi, ctx->theta, ctx->m, ctx->v, ctx->theta_b,
+                                             ctx->m_b, ctx->v_b, ctx->w16, ctx->st, ctx->sc, ctx->flag);
+    else
+        k12_fused<false><<<grid, 256, 0, s>>>(ctx->acc, P, count, lo, hi, ctx->theta, ctx->m, ctx->v, ctx->theta_b,
+                                              ctx->m_b, ctx->v_b, ctx->w16, ctx->st, ctx->sc, ctx->flag);
+    CKL("k12_fused");
+    return SMPU_OK;
+}
+
+// host memory: double-buffered H2D staging on the copy stream, overlapped with `launch(stage, c0, c1)` on `s`
+// (the staging buffer holds elements [c0, c1))
+template <class Launch>
+smpu_status staged(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, cudaStream_t s, Launch launch) {
+    for (int64_t c0 = lo; c0 < hi; c0 += kStageElems) {
+        int64_t c1 = c0 + kStageElems < hi ? c0 + kStageElems : hi;
+        int j = (int)(ctx->stage_count++ & 1);
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->stage_free[j], 0));
+        CK(cudaMemcpyAsync(ctx->stage[j], src + (c0 - lo), (size_t)(c1 - c0) * 2, cudaMemcpyHostToDevice,
+                           ctx->copy_stream));
+        CK(cudaEventRecord(ctx->stage_full[j], ctx->copy_stream));
+        CK(cudaStreamWaitEvent(s, ctx->stage_full[j], 0));
+        smpu_status st = launch((const uint16_t*)ctx->stage[j], c0, c1);
+        if (st != SMPU_OK) return st;
+        CK(cudaEventRecord(ctx->stage_free[j], s));
+    }
+    return SMPU_OK;
+}
+
+// accumulate src (host or device) into acc[lo, hi); fuse: the last micro-batch at W = 1 with fuse_final, whose
+// elements go straight into Adam (launch_k12) instead
 smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, bool first, bool detect,
-                             cudaStream_t s, bool stats = false) {
+                             cudaStream_t s, bool stats = false, bool fuse = false) {
+    if (fuse) {
+        if (!src) return launch_k12(ctx, nullptr, 0, lo, hi, true, s);
+        if (classify(src) == PTR_DEVICE) return launch_k12(ctx, &src, 1, lo, hi, !first, s);
+        return staged(ctx, src, lo, hi, s, [&](const uint16_t* g, int64_t c0, int64_t c1) {
+            return launch_k12(ctx, &g, 1, c0, c1, !first, s);
+        });
+    }
     if (!src) {
         // accumulated in place by the producer (smpu_accumulator): only the last micro-batch's
         // overflow test / statistic remains to be done
@@ -358,21 +418,9 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
         return SMPU_OK;
     }
     if (classify(src) == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s, stats);
-    // host memory: double-buffered H2D staging on the copy stream, overlapped with K1 on `s`
-    for (int64_t c0 = lo; c0 < hi; c0 += kStageElems) {
-        int64_t c1 = c0 + kStageElems < hi ? c0 + kStageElems : hi;
-        int j = (int)(ctx->stage_count++ & 1);
-        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->stage_free[j], 0));
-        CK(cudaMemcpyAsync(ctx->stage[j], src + (c0 - lo), (size_t)(c1 - c0) * 2, cudaMemcpyHostToDevice,
-                           ctx->copy_stream));
-        CK(cudaEventRecord(ctx->stage_full[j], ctx->copy_stream));
-        CK(cudaStreamWaitEvent(s, ctx->stage_full[j], 0));
-        // the staging buffer holds elements [c0, c1): index it relative to c0
-        smpu_status st = launch_k1(ctx, ctx->stage[j], c0, c1, first, detect, s, stats);
-        if (st != SMPU_OK) return st;
-        CK(cudaEventRecord(ctx->stage_free[j], s));
-    }
-    return SMPU_OK;
+    return staged(ctx, src, lo, hi, s, [&](const uint16_t* g, int64_t c0, int64_t c1) {
+        return launch_k1(ctx, g, c0, c1, first, detect, s, stats);
+    });
 }
 
 smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t cs) {
@@ -455,9 +503,6 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
 // (k0_early_lsa through peer memory, or k0_early after a 16-byte NCCL all-reduce on a second communicator),
 // then Adam per bucket on its own stream, each bucket right behind its gradient all-reduce -- K2 overlaps the
 // remaining all-reduces.
-// token count source of the decision kernels: kernel argument, or tok_dev inside a captured graph
-const int64_t* tok_src(const smpu_ctx* ctx) { return ctx->capturing ? ctx->tok_dev : nullptr; }
-
 smpu_status launch_decision_lsa(smpu_ctx* ctx, cudaStream_t ds) {
 #define SMPU_DEC(WW)                                                                                             \
     k0_early_lsa<WW><<<1, 32, 0, ds>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->stat,                     \
@@ -547,6 +592,9 @@ void free_ctx(smpu_ctx* c) {
     cudaFree(c->theta);
     cudaFree(c->m);
     cudaFree(c->v);
+    cudaFree(c->theta_b);
+    cudaFree(c->m_b);
+    cudaFree(c->v_b);
     if (!c->acc_from_nccl) cudaFree(c->w16);
     if (c->acc_from_nccl) ncclMemFree(c->acc);
     else cudaFree(c->acc);
@@ -613,6 +661,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->bucket_bytes = int64_t(150) << 20;
     c->allreduce = SMPU_AR_AUTO;
     c->sharded = 0;
+    c->fuse_final = 1;
     return SMPU_OK;
 }
 
@@ -698,6 +747,12 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMalloc(&ctx->theta, n * 4));
     IK(cudaMalloc(&ctx->m, n * 4));
     IK(cudaMalloc(&ctx->v, n * 4));
+    ctx->fused = world == 1 && cfg->fuse_final != 0;
+    if (ctx->fused) {
+        IK(cudaMalloc(&ctx->theta_b, n * 4));
+        IK(cudaMalloc(&ctx->m_b, n * 4));
+        IK(cudaMalloc(&ctx->v_b, n * 4));
+    }
 
     const size_t acc_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
@@ -783,6 +838,11 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMemcpyAsync(ctx->theta, init_params, n * 4, cudaMemcpyDefault, s0));
     IK(cudaMemsetAsync(ctx->m, 0, n * 4, s0));
     IK(cudaMemsetAsync(ctx->v, 0, n * 4, s0));
+    if (ctx->fused) {
+        IK(cudaMemsetAsync(ctx->theta_b, 0, n * 4, s0));
+        IK(cudaMemsetAsync(ctx->m_b, 0, n * 4, s0));
+        IK(cudaMemsetAsync(ctx->v_b, 0, n * 4, s0));
+    }
     IK(cudaMemsetAsync(ctx->acc, 0, n * 2, s0));
     IK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), s0));
     IK(cudaMemsetAsync(ctx->stat, 0, sizeof(uint32_t), s0));
@@ -985,7 +1045,7 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
     const bool first = ctx->micro == 1;
     const bool multi = last && ctx->world > 1;
     st = accumulate_range(ctx, (const uint16_t*)grads, ctx->bbegin[bucket], ctx->bbegin[bucket + 1], first,
-                          last && ctx->world == 1, s, multi);
+                          last && ctx->world == 1 && !ctx->fused, s, multi, last && ctx->fused);
     if (st != SMPU_OK) return st;
     ctx->bucket_done[bucket] = 1;
     if (multi) {
@@ -1026,7 +1086,8 @@ smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, v
     if (st != SMPU_OK) return st;
     start_micro(ctx, ntokens);
     const bool last = final_micro(ctx);
-    st = accumulate_range(ctx, (const uint16_t*)grads, 0, ctx->n, ctx->micro == 1, last, s);
+    st = accumulate_range(ctx, (const uint16_t*)grads, 0, ctx->n, ctx->micro == 1, last && !ctx->fused, s, false,
+                          last && ctx->fused);
     if (st != SMPU_OK) return st;
     return leave_stream(ctx, s);
 }
@@ -1067,7 +1128,8 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const 
         if (st != SMPU_OK) return st;
         return issue_decision(ctx);
     }
-    st = launch_k1_many(ctx, g, count, 0, ctx->n, first, last, false, s);
+    st = last && ctx->fused ? launch_k12(ctx, g, count, 0, ctx->n, !first, s)
+                            : launch_k1_many(ctx, g, count, 0, ctx->n, first, last, false, s);
     if (st != SMPU_OK) return st;
     return leave_stream(ctx, s);
 }
@@ -1171,11 +1233,26 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
             smpu_status st2 = launch_k2(ctx, 0, ctx->n, DEC_APPLY_LATE, s);
             if (st2 != SMPU_OK) return st2;
         }
+    } else if (ctx->fused) {
+        // the update already ran speculatively into the other bank (k12_fused): decide, make that bank current
+        // if R was finite, else re-cast w16 from the current theta
+        {
+            Timed t(ctx, SMPU_K0, s);
+            k0_decide<<<1, 32, 0, s>>>(ctx->flag, ctx->local_tokens, tok_src(ctx), ctx->st, ctx->sc, ctx->scale,
+                                       ctx->ring_dev, (int)(kRing - 1), ctx->dcfg, 1);
+            CKL("k0_decide");
+        }
+        {
+            Timed t(ctx, SMPU_KCAST, s);
+            kc_restore<<<ctx->grid_k1s, 256, 0, s>>>(ctx->theta, ctx->theta_b, ctx->st, ctx->sc, ctx->w16, ctx->n);
+            CKL("kc_restore");
+        }
+        ctx->fused_prepped = false;
     } else {
         {
             Timed t(ctx, SMPU_K0, s);
             cudaError_t e = launch_pdl(ctx, k0_decide, 1, 32, s, ctx->flag, ctx->local_tokens, tok_src(ctx), ctx->st,
-                                       ctx->sc, ctx->scale, ctx->ring_dev, (int)(kRing - 1), ctx->dcfg);
+                                       ctx->sc, ctx->scale, ctx->ring_dev, (int)(kRing - 1), ctx->dcfg, 0);
             if (e != cudaSuccess) return fail_cuda(ctx, e, "k0_decide", __LINE__);
             CKL("k0_decide");
         }
@@ -1236,7 +1313,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     smpu_status st = SMPU_OK;
     cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
     if (e == cudaSuccess) {
-        if (ctx->cfg.update_freq == 1 && ctx->world == 1 && ctx->k2_oneshot) {
+        if (ctx->cfg.update_freq == 1 && ctx->world == 1 && ctx->k2_oneshot && !ctx->fused) {
             // c = 1, W = 1: R = g_1.  The buffer is fixed and read at replay, so nothing needs copying: test it
             // for overflow in place (2 B/elem) and let Adam read it directly -- 30 instead of 32 B/elem.
             // (The accumulator, smpu_get_state(ACCUM), is then left untouched by these replays.)
@@ -1262,6 +1339,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     }
     ctx->capturing = false;
     ctx->timing = timing;
+    ctx->fused_prepped = false;
     for (int k = 0; k < SMPU_N_KERNELS; ++k) {
         ctx->graph_launches[k] = ctx->launches[k] - before[k];
         ctx->launches[k] = before[k];
@@ -1308,11 +1386,15 @@ smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, 
     return leave_stream(ctx, s);
 }
 
+// the ctx's device is current and its work complete (the bank of a fused ctx is read from the device)
 static smpu_status state_array(smpu_ctx* ctx, int which, void** p, int64_t* bytes) {
+    int64_t bank = 0;
+    if (ctx->fused && which >= SMPU_STATE_MASTER && which <= SMPU_STATE_V)
+        CK(cudaMemcpy(&bank, &ctx->st->bank, sizeof bank, cudaMemcpyDeviceToHost));
     switch (which) {
-        case SMPU_STATE_MASTER: *p = ctx->theta; *bytes = ctx->n * 4; break;
-        case SMPU_STATE_M: *p = ctx->m; *bytes = ctx->n * 4; break;
-        case SMPU_STATE_V: *p = ctx->v; *bytes = ctx->n * 4; break;
+        case SMPU_STATE_MASTER: *p = bank ? ctx->theta_b : ctx->theta; *bytes = ctx->n * 4; break;
+        case SMPU_STATE_M: *p = bank ? ctx->m_b : ctx->m; *bytes = ctx->n * 4; break;
+        case SMPU_STATE_V: *p = bank ? ctx->v_b : ctx->v; *bytes = ctx->n * 4; break;
         case SMPU_STATE_W16: *p = ctx->w16; *bytes = ctx->n * 2; break;
         case SMPU_STATE_ACCUM: *p = ctx->acc; *bytes = ctx->n * 2; break;
         case SMPU_STATE_SCALARS: *p = ctx->st; *bytes = 4 * sizeof(int64_t); break;
@@ -1324,13 +1406,13 @@ static smpu_status state_array(smpu_ctx* ctx, int which, void** p, int64_t* byte
 smpu_status smpu_get_state(smpu_ctx* ctx, int which, void* dst, int64_t bytes) {
     LIVE(ctx);
     if (!dst) return set_err(SMPU_EINVAL, "null dst");
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
     void* p;
     int64_t nb;
     smpu_status s = state_array(ctx, which, &p, &nb);
     if (s != SMPU_OK) return s;
     if (bytes != nb) return set_err(SMPU_EINVAL, "state %d is %lld bytes, got %lld", which, (long long)nb, (long long)bytes);
-    CK(cudaSetDevice(ctx->dev));
-    CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(dst, p, (size_t)nb, cudaMemcpyDefault));
     return SMPU_OK;
 }
@@ -1339,13 +1421,13 @@ smpu_status smpu_set_state(smpu_ctx* ctx, int which, const void* src, int64_t by
     LIVE(ctx);
     if (!src) return set_err(SMPU_EINVAL, "null src");
     if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_set_state in the middle of an update");
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
     void* p;
     int64_t nb;
     smpu_status s = state_array(ctx, which, &p, &nb);
     if (s != SMPU_OK) return s;
     if (bytes != nb) return set_err(SMPU_EINVAL, "state %d is %lld bytes, got %lld", which, (long long)nb, (long long)bytes);
-    CK(cudaSetDevice(ctx->dev));
-    CK(cudaDeviceSynchronize());
     if (which == SMPU_STATE_SCALARS) {
         int64_t v[4];
         memcpy(v, src, sizeof v);

@@ -18,9 +18,9 @@ LIB_PATH = os.path.join(_PKG, "libsmpu.so")
 
 OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EPOISONED = range(7)
 STATE_MASTER, STATE_M, STATE_V, STATE_W16, STATE_ACCUM, STATE_SCALARS = range(6)
-K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, DECISION_AR, K1_MANY, N_KERNELS = range(10)
+K1_FIRST, K1_ADD, K1S, K0, K2, KCAST, ALLREDUCE, DECISION_AR, K1_MANY, K12, N_KERNELS = range(11)
 KERNEL_NAMES = ["k1_first", "k1_add", "k1s_sweep", "k0_decide", "k2_adam", "kc_cast", "allreduce", "decision_ar",
-                "k1_many"]
+                "k1_many", "k12_fused"]
 GRAPH_STREAMING, GRAPH_RESIDENT = 0, 1
 STREAM_NAMES = ["caller", "allreduce", "decision", "adam_per_bucket"]
 AR_AUTO, AR_NCCL, AR_FUSED = range(3)
@@ -38,7 +38,8 @@ class Config(ctypes.Structure):
                 ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("init_scale_log2", ctypes.c_int32),
                 ("min_scale_log2", ctypes.c_int32), ("max_scale_log2", ctypes.c_int32),
                 ("growth_interval", ctypes.c_int64), ("update_freq", ctypes.c_int32),
-                ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32), ("sharded", ctypes.c_int32)]
+                ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32), ("sharded", ctypes.c_int32),
+                ("fuse_final", ctypes.c_int32)]
 
 
 class StepResult(ctypes.Structure):

@@ -38,8 +38,9 @@ def test_every_declared_symbol_is_exported(P):
 
 
 def test_abi_version_and_defaults(P):
-    assert P.abi_version() == 1
+    assert P.abi_version() == 2
     c = P.config_default()
+    assert (c.allreduce, c.sharded, c.fuse_final) == (0, 0, 1)
     assert (c.peak_lr, c.warmup_updates, c.beta1, c.beta2, c.eps) == (5e-4, 4000, 0.9, 0.98, 1e-8)
     assert (c.init_scale_log2, c.min_scale_log2, c.max_scale_log2, c.growth_interval) == (7, -5, 24, 2000)
     assert c.bucket_bytes == 150 << 20                                                                # P:212 fn
@@ -102,3 +103,13 @@ def test_sched_library_exports_header():
     lib = ctypes.CDLL(so)
     for name in names:
         assert hasattr(lib, name), name
+
+
+def test_kernel_ids_match_header(P):
+    """The binding's kernel-id table is the header's enum (smpu_kernel_stats indexes by it)."""
+    hdr = open(os.path.join(ROOT, "include", "smpu.h")).read()
+    ids = {m.group(1): int(m.group(2)) for m in re.finditer(r"SMPU_(K\w+|ALLREDUCE|DECISION_AR|N_KERNELS) = (\d+)", hdr)}
+    assert ids["N_KERNELS"] == P.smpu.N_KERNELS == len(P.smpu.KERNEL_NAMES)
+    for name, k in ids.items():
+        if name != "N_KERNELS":
+            assert getattr(P.smpu, name) == k, name

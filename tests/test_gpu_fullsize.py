@@ -47,7 +47,8 @@ def test_base_ende_full_vector(P):
     lay = synth.Layout(wl)
     theta0 = torch.empty(lay.n, dtype=torch.float32, device="cuda")
     synth.theta0_gpu(theta0, wl)
-    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))                  # default: fused last micro-batch
+    ref = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, fuse_final=0))     # stores R: checked bitwise
     th0 = synth.theta0_cpu(wl, lay)
     assert np.array_equal(theta0.cpu().numpy(), th0)
     orc = O.Oracle(th0)
@@ -59,12 +60,17 @@ def test_base_ende_full_vector(P):
         tok = synth.ntokens(wl, u, 0, 1)
         step.accumulate(buf[0], tok)
         res = step.step()
+        ref.accumulate(buf[0], tok)
+        rres = ref.step()
         before = snapshot(orc)
         ores = orc.update([[synth.micro_grad_cpu(wl, lay, u, 0, 1, e)]], [[tok]])
-        assert decisions(res) == oracle_decisions(ores)
-        assert np.array_equal(step.get_state(P.smpu.STATE_ACCUM), ores["R"])
+        assert decisions(res) == decisions(rres) == oracle_decisions(ores)
+        assert np.array_equal(ref.get_state(P.smpu.STATE_ACCUM), ores["R"])
         mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
-        check_state(gpu_state(step), snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
+        got = gpu_state(step)
+        check_state(got, snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
+        for name, arr in gpu_state(ref).items():
+            assert np.array_equal(got[name], arr), f"update {u}: fused {name} differs from the unfused path"
 
 
 @pytest.mark.parametrize("final", ["whole", "bucket"])
@@ -76,7 +82,8 @@ def test_big_ende_sampled(P, final):
     lay = synth.Layout(wl)
     theta0 = torch.empty(lay.n, dtype=torch.float32, device="cuda")
     synth.theta0_gpu(theta0, wl)
-    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, fuse_final=0))   # stores R: checked (sampled) bitwise
+    fstep = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))                # the default, fused last micro-batch
     assert step.n_buckets == 3
     idx = _sample_idx(lay, step.bucket_begin, extra=[123_456_789])
     orc = O.Oracle(synth.theta0_sample(wl, idx))
@@ -86,15 +93,17 @@ def test_big_ende_sampled(P, final):
         e = orc.e
         _gpu_inputs(wl, lay, u, 0, e, bufs)
         toks = [synth.ntokens(wl, u, 0, k) for k in range(1, wl.update_freq + 1)]
-        for k in range(wl.update_freq):
-            if final == "bucket" and k == wl.update_freq - 1:
-                step.micro_begin(toks[k])
-                bb = step.bucket_begin
-                for b in (2, 0, 1):
-                    step.accumulate_bucket(b, bufs[k][bb[b]:bb[b + 1]])
-            else:
-                step.accumulate(bufs[k], toks[k])
+        for st in (step, fstep):
+            for k in range(wl.update_freq):
+                if final == "bucket" and k == wl.update_freq - 1:
+                    st.micro_begin(toks[k])
+                    bb = st.bucket_begin
+                    for b in (2, 0, 1):
+                        st.accumulate_bucket(b, bufs[k][bb[b]:bb[b + 1]])
+                else:
+                    st.accumulate(bufs[k], toks[k])
         res = step.step()
+        assert decisions(fstep.step()) == decisions(res), u
         grads = [[synth.micro_grad_sample(wl, lay, idx, u, 0, k, e) for k in range(1, wl.update_freq + 1)]]
         overflow = O.full_overflow(wl, lay, u, e) if u == 1 else (u == 2)
         before = snapshot(orc)
@@ -106,7 +115,10 @@ def test_big_ende_sampled(P, final):
         assert np.array_equal(acc[~fin] & 0x7C00, ores["R"][~fin] & 0x7C00)
         if ores["applied"]:
             mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
-        check_state(gpu_state(step, idx), snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
+        got = gpu_state(step, idx)
+        check_state(got, snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
+        for name, arr in gpu_state(fstep, idx).items():
+            assert np.array_equal(got[name], arr), f"update {u}: fused {name} differs from the unfused path"
 
 
 def test_big_enfr_5200_updates_periodic_overflow(P, gold):

@@ -1,7 +1,8 @@
 """Randomised parity (hypothesis, fixed seed): random tensor lists (sizes 1..40k, every class), update_freq 1..5,
 bucket thresholds from a few bytes to 1 MiB, every accumulation entry point (whole / bucket-wise in a random
-order / resident accumulate_many / in-place NULL / CUDA graph), injected non-finites anywhere; the library vs the
-oracle on decisions (bitwise), the accumulator (bitwise) and theta/m/v/w16 (tolerance), every update."""
+order / resident accumulate_many / in-place NULL / CUDA graph), fuse_final on or off, injected non-finites
+anywhere; the library vs the oracle on decisions (bitwise), the accumulator (bitwise, wherever it holds R) and
+theta/m/v/w16 (tolerance), every update."""
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, seed, settings
@@ -34,7 +35,8 @@ def cases(draw):
     mode = draw(st.sampled_from(["whole", "bucket", "many", "inplace", "graph"]))
     bucket_bytes = draw(st.sampled_from([2, 1000, 16_384, 100_000, 1 << 20]))
     order_seed = draw(st.integers(0, 1000))
-    return tensors, c, inj, mode, bucket_bytes, order_seed
+    fuse = draw(st.booleans())
+    return tensors, c, inj, mode, bucket_bytes, order_seed, fuse
 
 
 @seed(20261018)
@@ -43,11 +45,11 @@ def cases(draw):
 def test_fuzz_against_oracle(case):
     import torch
     import paper_1806_00187_b200 as P
-    tensors, c, inj, mode, bucket_bytes, order_seed = case
+    tensors, c, inj, mode, bucket_bytes, order_seed, fuse = case
     wl = models.Workload("fuzz", tensors, 1, c, injections=inj)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
-    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=bucket_bytes))
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=bucket_bytes, fuse_final=int(fuse)))
     orc = O.Oracle(theta0)
     mags = Magnitudes(theta0)
     rng = np.random.default_rng(order_seed)
@@ -84,7 +86,9 @@ def test_fuzz_against_oracle(case):
                         step.accumulate_bucket(int(b), dev[k][bb[b]:bb[b + 1]])
             res = step.step()
         assert decisions(res) == oracle_decisions(ores), (case, u)
-        if mode != "graph" or c > 1:
+        # R is stored unless the last micro-batch was fused into Adam (an in-place producer stores it itself)
+        # or the unfused c = 1 graph let Adam read the producer's buffer
+        if (not fuse or mode == "inplace") and (mode != "graph" or c > 1 or fuse):
             got = step.get_state(P.smpu.STATE_ACCUM)
             R = ores["R"]
             fin = (R & 0x7C00) != 0x7C00
