@@ -35,7 +35,10 @@ def main():
     wlW = models.Workload("winv", tensors, world, 1)
     multi = P.UpdateStep(wl1.numel, theta0, lib_cfg(wlW, bucket_bytes=300_000, allreduce=P.smpu.AR_FUSED),
                          world=world, rank=rank, nccl_id=obj[0], device=local)
-    single = P.UpdateStep(wl1.numel, theta0, lib_cfg(wl1, bucket_bytes=300_000)) if rank == 0 else None
+    # (1, c = W) twice: unfused, whose accumulator holds R like the multi-rank ctx's, and the default fused
+    # last micro-batch (R consumed without being stored: compared on theta/m/v/w16)
+    single = P.UpdateStep(wl1.numel, theta0, lib_cfg(wl1, bucket_bytes=300_000, fuse_final=0)) if rank == 0 else None
+    fused = P.UpdateStep(wl1.numel, theta0, lib_cfg(wl1, bucket_bytes=300_000)) if rank == 0 else None
     failures = []
     e = 7
     for u in range(1, 7):
@@ -46,17 +49,21 @@ def main():
         if rank == 0:
             for j in range(world):
                 single.accumulate(h2t(micro[j]), toks[j])
-            rs = single.step()
-            if decisions(rm) != decisions(rs):
-                failures.append(f"update {u}: decisions {decisions(rm)} vs {decisions(rs)}")
+                fused.accumulate(h2t(micro[j]), toks[j])
+            rs, rf = single.step(), fused.step()
+            if not decisions(rm) == decisions(rs) == decisions(rf):
+                failures.append(f"update {u}: decisions {decisions(rm)} vs {decisions(rs)} vs {decisions(rf)}")
             for w in range(5):
                 if not np.array_equal(multi.get_state(w), single.get_state(w)):
                     failures.append(f"update {u}: state {w} differs between (W={world}, c=1) and (1, c={world})")
+                if w < 4 and not np.array_equal(multi.get_state(w), fused.get_state(w)):
+                    failures.append(f"update {u}: state {w} differs between (W={world}, c=1) and fused (1, c={world})")
         e = rm["scale_log2_next"]
     fl = [None] * world
     dist.all_gather_object(fl, failures)
     if single is not None:
         single.close()
+        fused.close()
     multi.close()
     dist.destroy_process_group()
     allf = [f for x in fl for f in x]
