@@ -15,7 +15,8 @@
  *
  * Conventions for every call
  *  - Pointers marked "device" are CUDA device pointers of the ctx's device; "host or device" pointers
- *    are classified with cudaPointerGetAttributes (pinned or pageable host memory is accepted).
+ *    are classified with cudaPointerGetAttributes (pinned or pageable host memory is accepted).  Device
+ *    memory of another GPU is refused with SMPU_EINVAL.
  *  - `stream` arguments are cudaStream_t values passed as void*; NULL means the legacy default stream.
  *    Reads of caller buffers are stream-ordered on that stream: the caller may reuse a buffer after
  *    later work on the same stream.  Different calls may use different streams; the library orders its

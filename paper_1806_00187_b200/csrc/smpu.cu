@@ -48,7 +48,7 @@ smpu_status set_err(smpu_status s, const char* fmt, ...) {
     return s;
 }
 
-enum PtrKind { PTR_DEVICE, PTR_HOST };
+enum PtrKind { PTR_DEVICE, PTR_HOST, PTR_FOREIGN };   // FOREIGN: device memory of another GPU
 
 }  // namespace
 
@@ -186,13 +186,15 @@ smpu_status fail_nccl(smpu_ctx* c, ncclResult_t e, const char* what, int line) {
         default: return set_err(SMPU_EINVAL, what " supports 2..8 ranks"); \
     }
 
-PtrKind classify(const void* p) {
+PtrKind classify(const smpu_ctx* c, const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return PTR_HOST;
     }
-    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? PTR_DEVICE : PTR_HOST;
+    if (a.type == cudaMemoryTypeManaged) return PTR_DEVICE;
+    if (a.type == cudaMemoryTypeDevice) return a.device == c->dev ? PTR_DEVICE : PTR_FOREIGN;
+    return PTR_HOST;
 }
 
 cudaEvent_t pool_event(smpu_ctx* c) {
@@ -401,7 +403,9 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
                              cudaStream_t s, bool stats = false, bool fuse = false) {
     if (fuse) {
         if (!src) return launch_k12(ctx, nullptr, 0, lo, hi, true, s);
-        if (classify(src) == PTR_DEVICE) return launch_k12(ctx, &src, 1, lo, hi, !first, s);
+        const PtrKind kind = classify(ctx, src);
+        if (kind == PTR_FOREIGN) return set_err(SMPU_EINVAL, "micro-gradients on another device than the ctx's");
+        if (kind == PTR_DEVICE) return launch_k12(ctx, &src, 1, lo, hi, !first, s);
         return staged(ctx, src, lo, hi, s, [&](const uint16_t* g, int64_t c0, int64_t c1) {
             return launch_k12(ctx, &g, 1, c0, c1, !first, s);
         });
@@ -417,7 +421,9 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
         CKL("k1_scan");
         return SMPU_OK;
     }
-    if (classify(src) == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s, stats);
+    const PtrKind kind = classify(ctx, src);
+    if (kind == PTR_FOREIGN) return set_err(SMPU_EINVAL, "micro-gradients on another device than the ctx's");
+    if (kind == PTR_DEVICE) return launch_k1(ctx, src, lo, hi, first, detect, s, stats);
     return staged(ctx, src, lo, hi, s, [&](const uint16_t* g, int64_t c0, int64_t c1) {
         return launch_k1(ctx, g, c0, c1, first, detect, s, stats);
     });
@@ -1038,6 +1044,8 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
     if (bucket < 0 || bucket >= ctx->nb) return set_err(SMPU_EINVAL, "bucket %d out of [0, %d)", bucket, ctx->nb);
     if (ctx->bucket_done[bucket]) return set_err(SMPU_ESTATE, "bucket %d already given in this micro-batch", bucket);
     CK(cudaSetDevice(ctx->dev));
+    if (grads && classify(ctx, grads) == PTR_FOREIGN)
+        return set_err(SMPU_EINVAL, "bucket gradients on another device than the ctx's (%d)", ctx->dev);
     cudaStream_t s = (cudaStream_t)stream;
     smpu_status st = enter_stream(ctx, s);
     if (st != SMPU_OK) return st;
@@ -1069,6 +1077,8 @@ smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, v
     if (ctx->micro >= ctx->cfg.update_freq)
         return set_err(SMPU_ESTATE, "already %d micro-batches this update; call smpu_step", ctx->micro);
     CK(cudaSetDevice(ctx->dev));
+    if (grads && classify(ctx, grads) == PTR_FOREIGN)
+        return set_err(SMPU_EINVAL, "micro-gradients on another device than the ctx's (%d)", ctx->dev);
     cudaStream_t s = (cudaStream_t)stream;
     if (ctx->micro + 1 == ctx->cfg.update_freq && ctx->world > 1) {
         // final micro-batch of a multi-GPU update: bucket by bucket, so that bucket b's all-reduce
@@ -1104,7 +1114,7 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const 
     const uint16_t* g[kMaxMany];
     for (int k = 0; k < count; ++k) {
         if (ntokens[k] < 0) return set_err(SMPU_EINVAL, "ntokens[%d] < 0", k);
-        if (!grads[k] || classify(grads[k]) != PTR_DEVICE)
+        if (!grads[k] || classify(ctx, grads[k]) != PTR_DEVICE)
             return set_err(SMPU_EINVAL, "micro_grads[%d] must be a device buffer", k);
         g[k] = (const uint16_t*)grads[k];
     }
@@ -1294,7 +1304,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
                                     "of captured NCCL collectives on two communicators hung on B200 (2 ranks)");
     CK(cudaSetDevice(ctx->dev));
     for (int k = 0; k < count; ++k)
-        if (!micro_grads[k] || classify(micro_grads[k]) != PTR_DEVICE)
+        if (!micro_grads[k] || classify(ctx, micro_grads[k]) != PTR_DEVICE)
             return set_err(SMPU_EINVAL, "micro_grads[%d] must be a device buffer for graph capture", k);
     if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     if (ctx->graph_exec) {

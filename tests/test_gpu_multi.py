@@ -128,3 +128,28 @@ def test_allreduce_accumulator_primitive(impl):
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-3000:], p.stderr[-3000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+def test_foreign_device_buffer_rejected():
+    """A micro-gradient on another GPU than the ctx's is EINVAL, before any state changes (include/smpu.h)."""
+    import numpy as np
+    import torch
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_1806_00187_b200 as P
+    import synth
+    from synth import models
+    from tests.gpu_util import lib_cfg
+    wl = models.Workload("foreign", [("w", 10_000, 0)], 1, 2)
+    lay = synth.Layout(wl)
+    step = P.UpdateStep(wl.numel, synth.theta0_cpu(wl, lay), lib_cfg(wl), device=0)
+    g1 = torch.zeros(lay.n, dtype=torch.int16, device="cuda:1")
+    with pytest.raises(P.SmpuError) as ei:
+        step.accumulate(g1, 10)
+    assert ei.value.status == P.smpu.EINVAL
+    g0 = torch.zeros(lay.n, dtype=torch.int16, device="cuda:0")
+    step.accumulate(g0, 10)                   # the ctx is unchanged: still two micro-batches to go
+    step.accumulate(g0, 10)
+    assert step.step()["applied"] == 1
+    assert np.isfinite(step.get_master()).all()
+    step.close()
