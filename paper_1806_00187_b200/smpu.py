@@ -137,10 +137,10 @@ def _ptr(x):
     raise TypeError(type(x))
 
 
-def _stream(s):
-    if s is None:
+def _stream(s, device: int):
+    if s is None:                  # torch's current stream on the ctx's device (not on torch's current device)
         import torch
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
     if isinstance(s, int):
         return ctypes.c_void_p(s)
     return ctypes.c_void_p(s.cuda_stream)
@@ -196,30 +196,30 @@ class UpdateStep:
 
     # -------------------------------------------------------------- hot path
     def accumulate(self, micro_grads, ntokens: int, stream=None):
-        _check(lib().smpu_accumulate(self._ctx, _ptr(micro_grads), int(ntokens), _stream(stream)))
+        _check(lib().smpu_accumulate(self._ctx, _ptr(micro_grads), int(ntokens), _stream(stream, self.device)))
 
     def micro_begin(self, ntokens: int):
         _check(lib().smpu_micro_begin(self._ctx, int(ntokens)))
 
     def accumulate_bucket(self, bucket: int, bucket_grads, stream=None):
-        _check(lib().smpu_accumulate_bucket(self._ctx, bucket, _ptr(bucket_grads), _stream(stream)))
+        _check(lib().smpu_accumulate_bucket(self._ctx, bucket, _ptr(bucket_grads), _stream(stream, self.device)))
 
     def tensor_ready(self, tensor: int, stream=None):
-        _check(lib().smpu_tensor_ready(self._ctx, tensor, _stream(stream)))
+        _check(lib().smpu_tensor_ready(self._ctx, tensor, _stream(stream, self.device)))
 
     def step(self, stream=None, wait: bool = True):
         """wait=True: returns the result dict; wait=False: asynchronous, returns None."""
         if not wait:
-            _check(lib().smpu_step(self._ctx, _stream(stream), None))
+            _check(lib().smpu_step(self._ctx, _stream(stream, self.device), None))
             return None
         r = StepResult()
-        _check(lib().smpu_step(self._ctx, _stream(stream), ctypes.byref(r)))
+        _check(lib().smpu_step(self._ctx, _stream(stream, self.device), ctypes.byref(r)))
         return r.as_dict()
 
     def accumulate_many(self, micro_grads, ntokens, stream=None):
         arr = (ctypes.c_void_p * len(micro_grads))(*[_ptr(g).value for g in micro_grads])
         toks = np.ascontiguousarray(ntokens, dtype=np.int64)
-        _check(lib().smpu_accumulate_many(self._ctx, arr, _ptr(toks), len(micro_grads), _stream(stream)))
+        _check(lib().smpu_accumulate_many(self._ctx, arr, _ptr(toks), len(micro_grads), _stream(stream, self.device)))
 
     def graph_capture(self, micro_grads, resident: bool = False):
         """Record update_freq x accumulate(micro_grads[k]) + step as one CUDA graph (device buffers);
@@ -229,10 +229,10 @@ class UpdateStep:
 
     def graph_launch(self, ntokens, stream=None):
         toks = np.ascontiguousarray(ntokens, dtype=np.int64)
-        _check(lib().smpu_graph_launch(self._ctx, _ptr(toks), toks.size, _stream(stream)))
+        _check(lib().smpu_graph_launch(self._ctx, _ptr(toks), toks.size, _stream(stream, self.device)))
 
     def allreduce_accumulator(self, stream=None):
-        _check(lib().smpu_allreduce_accumulator(self._ctx, _stream(stream)))
+        _check(lib().smpu_allreduce_accumulator(self._ctx, _stream(stream, self.device)))
 
     def result(self, attempt: int):
         r = StepResult()
