@@ -693,6 +693,22 @@ __global__ void __launch_bounds__(256, 4) k2_adam_1(float* __restrict__ theta, f
 // exactly K2's arithmetic (adam_unit / adam_elem).  Speculative: the overflow decision needs all of R, so the
 // update is computed from bank b of theta/m/v into bank 1-b and K0 makes it current only if R was finite; w16
 // is written in place and re-cast from the current bank on a skip (kc_restore).  R itself is never stored.
+// one element of K12 (heads, tails, misaligned buffers); returns the non-finite bit of R
+template <bool HAS_ACC>
+__device__ __forceinline__ uint32_t k12_elem(int64_t i, const uint16_t* __restrict__ acc, const ManyPtrs& P, int count,
+                                             int64_t lo, const float* ti, const float* mi, const float* vi, float* to,
+                                             float* mo, float* vo, uint16_t* __restrict__ w16, const Scalars& s) {
+    uint32_t x = HAS_ACC ? (uint32_t)acc[i] : (uint32_t)P.g[0][i - lo];
+    for (int k = HAS_ACC ? 0 : 1; k < count; ++k) x = hadd2_rn(x, (uint32_t)P.g[k][i - lo]) & 0xFFFFu;
+    float th = ti[i], mm = mi[i], vv = vi[i];
+    adam_elem(__half2float(__ushort_as_half((uint16_t)x)), th, mm, vv, s);
+    to[i] = th;
+    mo[i] = mm;
+    vo[i] = vv;
+    w16[i] = __half_as_ushort(__float2half_rn(th));
+    return h_nonfinite((uint16_t)x) ? 1u : 0u;
+}
+
 template <bool HAS_ACC>
 __global__ void __launch_bounds__(256, 4) k12_fused(const uint16_t* __restrict__ acc, ManyPtrs P, int count,
                                                     int64_t lo, int64_t hi, float* th0, float* m0, float* v0,
@@ -756,17 +772,83 @@ __global__ void __launch_bounds__(256, 4) k12_fused(const uint16_t* __restrict__
         st256(vo + i0, v);
         st128(w16 + i0, w16v);
     }
-    auto elem = [&](int64_t i) {
-        uint32_t x = HAS_ACC ? (uint32_t)acc[i] : (uint32_t)P.g[0][i - lo];
-        for (int k = HAS_ACC ? 0 : 1; k < count; ++k) x = hadd2_rn(x, (uint32_t)P.g[k][i - lo]) & 0xFFFFu;
-        if (h_nonfinite((uint16_t)x)) bad |= 1u;
-        float th = ti[i], mm = mi[i], vv = vi[i];
-        adam_elem(__half2float(__ushort_as_half((uint16_t)x)), th, mm, vv, s);
-        to[i] = th;
-        mo[i] = mm;
-        vo[i] = vv;
-        w16[i] = __half_as_ushort(__float2half_rn(th));
-    };
+    auto elem = [&](int64_t i) { bad |= k12_elem<HAS_ACC>(i, acc, P, count, lo, ti, mi, vi, to, mo, vo, w16, s); };
+    if (vec_ok) {
+        for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+        for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
+    }
+    raise_flag(bad != 0, flag);
+}
+
+// K12 over several resident micro-batches (smpu_accumulate_many's last call, count >= 4): 16-element units so
+// that every gradient load is 32 B and four of them are in flight per round, as in k1_accumulate_many; the sum
+// is then consumed by two 8-element Adam halves (theta/m/v are loaded only after the gradients, which keeps
+// the registers under the 4-CTA cap).  Same additions in the same order and the same Adam arithmetic.
+template <bool HAS_ACC>
+__global__ void __launch_bounds__(256, 4) k12_fused_many(const uint16_t* __restrict__ acc, ManyPtrs P, int count,
+                                                         int64_t lo, int64_t hi, float* th0, float* m0, float* v0,
+                                                         float* th1, float* m1, float* v1,
+                                                         uint16_t* __restrict__ w16, const DevState* __restrict__ st,
+                                                         const Scalars* __restrict__ scp, int* __restrict__ flag) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    bool vec_ok = true;
+    for (int k = 0; k < count; ++k) vec_ok &= ((reinterpret_cast<uintptr_t>(P.g[k] + (vbeg - lo)) & 31) == 0);
+    const int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0, vend = vbeg + nvec * 16;
+    const int k0 = HAS_ACC ? 0 : 1;
+    const int64_t i0 = vbeg + tid * 16, r0 = i0 - lo;
+    V8 x, y[4];
+    if (tid < nvec) {      // independent of the decision state and the bank: in flight while those are read
+        x = HAS_ACC ? ld256_ro(acc + i0) : ld256_ro(P.g[0] + r0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (k0 + j < count) y[j] = ld256_ro(P.g[k0 + j] + r0);
+    }
+    if (decision_of(scp) != DEC_APPLY) return;         // N = 0: the update is discarded
+    const Scalars s = *scp;
+    const bool b = st->bank != 0;
+    const float* __restrict__ ti = b ? th1 : th0;
+    const float* __restrict__ mi = b ? m1 : m0;
+    const float* __restrict__ vi = b ? v1 : v0;
+    float* __restrict__ to = b ? th0 : th1;
+    float* __restrict__ mo = b ? m0 : m1;
+    float* __restrict__ vo = b ? v0 : v1;
+    uint32_t bad = 0;
+    if (tid < nvec) {
+        for (int k = k0;; ) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < count) {
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) x.w[w] = hadd2_rn(x.w[w], y[j].w[w]);
+                }
+            k += 4;
+            if (k >= count) break;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < count) y[j] = ld256_ro(P.g[k + j] + r0);
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w) bad |= nonfinite_bits(x.w[w]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j0 = i0 + 8 * h;
+            V8 t = ld256_ro(ti + j0), m = ld256_ro(mi + j0), v = ld256_ro(vi + j0);
+            V4 xr, w16v;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) xr.w[w] = x.w[4 * h + w];
+            adam_unit(xr, t, m, v, w16v, s);
+            st256(to + j0, t);
+            st256(mo + j0, m);
+            st256(vo + j0, v);
+            st128(w16 + j0, w16v);
+        }
+    }
+    auto elem = [&](int64_t i) { bad |= k12_elem<HAS_ACC>(i, acc, P, count, lo, ti, mi, vi, to, mo, vo, w16, s); };
     if (vec_ok) {
         for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
         for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);

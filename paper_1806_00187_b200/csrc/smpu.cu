@@ -366,8 +366,21 @@ smpu_status launch_k12(smpu_ctx* ctx, const uint16_t* const* g, int count, int64
     if (hi <= lo) return SMPU_OK;
     ManyPtrs P;
     for (int k = 0; k < count; ++k) P.g[k] = g[k];
-    const int grid = grid_for((hi - lo + 7) / 8, 0x7fffffff);
     Timed t(ctx, SMPU_K12, s);
+    if (count >= 4) {     // resident micro-batches: 16-element units, four 32-B gradient loads in flight
+        const int gm = grid_for((hi - lo + 15) / 16, 0x7fffffff);
+        if (has_acc)
+            k12_fused_many<true><<<gm, 256, 0, s>>>(ctx->acc, P, count, lo, hi, ctx->theta, ctx->m, ctx->v,
+                                                    ctx->theta_b, ctx->m_b, ctx->v_b, ctx->w16, ctx->st, ctx->sc,
+                                                    ctx->flag);
+        else
+            k12_fused_many<false><<<gm, 256, 0, s>>>(ctx->acc, P, count, lo, hi, ctx->theta, ctx->m, ctx->v,
+                                                     ctx->theta_b, ctx->m_b, ctx->v_b, ctx->w16, ctx->st, ctx->sc,
+                                                     ctx->flag);
+        CKL("k12_fused_many");
+        return SMPU_OK;
+    }
+    const int grid = grid_for((hi - lo + 7) / 8, 0x7fffffff);
     if (has_acc)
         k12_fused<true><<<grid, 256, 0, s>>>(ctx->acc, P, count, lo, hi, ctx->theta, ctx->m, ctx->v, ctx->theta_b,
                                              ctx->m_b, ctx->v_b, ctx->w16, ctx->st, ctx->sc, ctx->flag);
