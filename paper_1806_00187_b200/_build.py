@@ -30,6 +30,8 @@ def build_smpu(verbose_ptxas=False):
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
     if verbose_ptxas:
         cmd += ["-Xptxas", "-v"]
+    if os.environ.get("SMPU_L2_HINT"):      # experiment builds only (kernels.cuh)
+        cmd += [f"-DSMPU_L2_HINT={int(os.environ['SMPU_L2_HINT'])}"]
     _run(cmd)
 
 

@@ -32,9 +32,24 @@ struct __align__(32) V8 { uint32_t w[8]; };   // 32 B: 16 halves or 8 floats
 struct __align__(16) V4 { uint32_t w[4]; };   // 16 B: 8 halves
 
 // ---------------------------------------------------------------------------------------------- memory ops
+// L2 cache-hint experiments (tools/experiments/l2_hints.sh): SMPU_L2_HINT=1 adds the 256-B L2 prefetch-size
+// hint to every 256-bit load, =2 marks every 256-bit load and store L2::evict_first.  Default: no hint.
+#ifndef SMPU_L2_HINT
+#define SMPU_L2_HINT 0
+#endif
+#if SMPU_L2_HINT == 1
+#define SMPU_LDH ".L2::256B"
+#define SMPU_STH ""
+#elif SMPU_L2_HINT == 2
+#define SMPU_LDH ".L2::evict_first"
+#define SMPU_STH ".L2::evict_first"
+#else
+#define SMPU_LDH ""
+#define SMPU_STH ""
+#endif
 __device__ __forceinline__ V8 ld256_ro(const void* p) {          // read-only for the whole kernel
     V8 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.nc.L1::no_allocate" SMPU_LDH ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
                    "=r"(r.w[6]), "=r"(r.w[7])
                  : "l"(p));
@@ -42,14 +57,14 @@ __device__ __forceinline__ V8 ld256_ro(const void* p) {          // read-only fo
 }
 __device__ __forceinline__ V8 ld256(const void* p) {             // read then written by the same thread
     V8 r;
-    asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.L1::no_allocate" SMPU_LDH ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
                    "=r"(r.w[6]), "=r"(r.w[7])
                  : "l"(p));
     return r;
 }
 __device__ __forceinline__ void st256(void* p, const V8& v) {
-    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+    asm volatile("st.global.L1::no_allocate" SMPU_STH ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
                  "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
                  : "memory");
 }
