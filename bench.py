@@ -662,10 +662,14 @@ def main_ours(args):
                                          "GPU, same run); library-only step (no backward to hide behind)"}
     if world > 1 and kstat["allreduce"]["ms"] > 0:
         ar_ms = kstat["allreduce"]["ms"] / args.steps
-        bus = 2 * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9
-        out["allreduce"] = {"impl": {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)), "ms_per_step": ar_ms,
+        # bus bytes per rank (nccl-tests convention): all-reduce 2(W-1)/W x 2n; the sharded layout's timed kernel is
+        # the reduce-scatter alone, (W-1)/W x 2n (its all-gather of w16 is peer stores inside the Adam kernel)
+        phases = 1 if args.sharded else 2
+        bus = phases * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9
+        out["allreduce"] = {"impl": {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)) +
+                            ("_reduce_scatter" if args.sharded else ""), "ms_per_step": ar_ms,
                             "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS,
-                            "frac_of_770_measured_peer": bus / 770.0}
+                            "frac_of_770_measured_peer": bus / 770.0, "in_situ": "concurrent with K1 / Adam"}
     if e2e:
         out["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:
