@@ -33,9 +33,14 @@
  * form + torch.optim.Adam in fp64; reduce S:390-393; large-batch equivalence
  * on a brute-force softmax-regression model.
  */
+#include <float.h>
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
+
+#if FLT_EVAL_METHOD != 0
+#error "orc_accumulate32 needs binary32 evaluation of float expressions (FLT_EVAL_METHOD 0)"
+#endif
 
 /* ------------------------------------------------------------------ binary16 codec
  * IEEE 754 binary16: 1 sign bit, 5 exponent bits (bias 15), 10 mantissa bits.
@@ -97,6 +102,25 @@ void orc_accumulate(uint16_t* A, const uint16_t* G, int64_t n, int first) {
     if (first) { memcpy(A, G, (size_t)n * 2); return; }
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) A[i] = orc_hadd(A[i], G[i]);
+}
+
+/* ------------------------------------------------------------------ fp32 accumulator variant (SURVEY Z1 knob)
+ * P:151 puts fwd/bwd and the all-reduce in FP16 but never names the accumulator (reading Z1 takes fp16, above).
+ * Variant: A32 = fp32(G_1); A32 = fl32(A32 + fp32(G_k)) for k = 2..c, binary32 round-to-nearest-even.  This is
+ * kept in binary32 (C float arithmetic: FLT_EVAL_METHOD 0, no contraction), not fp64, because the fp16 result
+ * depends on every binary32 rounding.  The rank's fp16 gradient is then rn16(A32), which enters the fp16 all-reduce
+ * unchanged.  Overflow stays "R holds a non-finite" (R4): a finite sum >= 65520 rounds to inf there. */
+void orc_accumulate32(float* A, const uint16_t* G, int64_t n, int first) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        float g = (float)orc_h2d(G[i]);   /* exact: binary16 is a subset of binary32 */
+        A[i] = first ? g : A[i] + g;
+    }
+}
+
+void orc_round16(uint16_t* out, const float* A, int64_t n) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = orc_d2h((double)A[i]);   /* one rounding: binary32 is exact in fp64 */
 }
 
 /* ------------------------------------------------------------------ all-reduce

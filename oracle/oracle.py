@@ -59,6 +59,8 @@ def lib():
         L.orc_h2d_array.argtypes = [p, p, i64]
         L.orc_d2h_array.argtypes = [p, p, i64]
         L.orc_accumulate.argtypes = [p, p, i64, i32]
+        L.orc_accumulate32.argtypes = [p, p, i64, i32]
+        L.orc_round16.argtypes = [p, p, i64]
         L.orc_reduce.argtypes = [p, p, i32, i64]
         L.orc_count_nonfinite.restype = i64
         L.orc_count_nonfinite.argtypes = [p, i64]
@@ -111,8 +113,17 @@ def lr_at(t: int, peak: float = 5e-4, warmup: int = 4000) -> float:
     return lib().orc_lr(t, peak, warmup)
 
 
-def accumulate(grads) -> np.ndarray:
-    """A = g_1, then A = rn16(A + g_k)."""
+def accumulate(grads, fp32: bool = False) -> np.ndarray:
+    """A = g_1, then A = rn16(A + g_k).  fp32: the Z1 variant, A32 = fp32(g_1), A32 = fl32(A32 + g_k),
+    returned as rn16(A32) (oracle.c orc_accumulate32)."""
+    if fp32:
+        A32 = np.empty(np.asarray(grads[0]).size, dtype=np.float32)
+        for k, g in enumerate(grads):
+            g = np.ascontiguousarray(g, dtype=np.uint16)
+            lib().orc_accumulate32(_p(A32), _p(g), A32.size, 1 if k == 0 else 0)
+        A = np.empty(A32.size, dtype=np.uint16)
+        lib().orc_round16(_p(A), _p(A32), A32.size)
+        return A
     A = np.empty_like(grads[0])
     for k, g in enumerate(grads):
         g = np.ascontiguousarray(g, dtype=np.uint16)
@@ -146,6 +157,7 @@ class Config:
     min_scale_log2: int = -5
     max_scale_log2: int = 24
     growth: int = 2000
+    accum_fp32: bool = False     # SURVEY Z1 knob: fp32 accumulator, rn16 before the fp16 all-reduce
 
     def c(self):
         return OrcCfg(self.peak_lr, self.warmup, self.beta1, self.beta2, self.eps, self.min_scale_log2,
@@ -179,7 +191,7 @@ class Oracle:
         full-vector decision is used (sampled mode)."""
         W, c = len(grads), len(grads[0])
         N = int(sum(sum(row) for row in ntokens))
-        A = [accumulate(grads[r]) for r in range(W)]
+        A = [accumulate(grads[r], self.cfg.accum_fp32) for r in range(W)]
         R = reduce(A)
         if overflow is None:
             overflow = count_nonfinite(R) > 0
@@ -202,14 +214,14 @@ class Oracle:
 
 
 # ----------------------------------------------------------------------------- workload drivers
-def full_overflow(wl, lay, u: int, e: int, chunk: int = 1 << 22) -> bool:
+def full_overflow(wl, lay, u: int, e: int, chunk: int = 1 << 22, accum_fp32: bool = False) -> bool:
     """Overflow decision of update u over the FULL vector, streamed in index chunks."""
     import synth
     W, c = wl.world, wl.update_freq
     for lo in range(0, lay.n, chunk):
         hi = min(lay.n, lo + chunk)
-        accs = [accumulate([synth.micro_grad_range(wl, lay, lo, hi, u, r, k, e) for k in range(1, c + 1)])
-                for r in range(W)]
+        accs = [accumulate([synth.micro_grad_range(wl, lay, lo, hi, u, r, k, e) for k in range(1, c + 1)],
+                           accum_fp32) for r in range(W)]
         if count_nonfinite(reduce(accs)) > 0:
             return True
     return False

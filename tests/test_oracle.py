@@ -102,6 +102,40 @@ def test_accumulate_and_reduce_brute_force():
     assert np.array_equal(O.reduce([a.view(np.uint16) for a in accs]), ref.view(np.uint16))
 
 
+def test_accumulate_fp32_variant_against_numpy_float32():
+    """SURVEY Z1 knob: A32 = fp32(g_1), A32 = fl32(A32 + g_k), then rn16.  Pinned to numpy's IEEE binary32 adds
+    and its float32 -> float16 conversion (round to nearest even), including non-finite inputs."""
+    rng = np.random.default_rng(11)
+    c, n = 6, 20000
+    g = rng.normal(0, 3000, (c, n)).astype(np.float16)
+    g[2, 17], g[4, 99], g[1, 5] = np.inf, np.nan, -np.inf
+    a = g[0].astype(np.float32)
+    for k in range(1, c):
+        a = (a + g[k].astype(np.float32)).astype(np.float32)
+    ref = a.astype(np.float16)
+    got = O.accumulate([g[k].view(np.uint16) for k in range(c)], fp32=True)
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got.view(np.float16)), nan)
+    assert np.array_equal(got[~nan], ref.view(np.uint16)[~nan])
+
+
+def test_accumulate_fp32_variant_special_cases():
+    """What the fp32 accumulator changes, worked by hand: an fp16 partial-sum overflow that cancels later
+    (40000 + 40000 - 29984: inf in fp16, 50016 in fp32); a sum reaching 65520 (rounds to inf in either);
+    small addends lost in fp16 but kept in fp32 (2048 + 1 + 1 = 2048 in fp16, 2050 in fp32); c = 1 is g_1."""
+    h = lambda *v: [np.asarray([x], dtype=np.float16).view(np.uint16) for x in v]  # noqa: E731
+    f16 = lambda a: float(a.view(np.float16)[0])  # noqa: E731
+    assert np.isinf(f16(O.accumulate(h(40000, 40000, -29984))))
+    assert f16(O.accumulate(h(40000, 40000, -29984), fp32=True)) == 50016.0
+    assert f16(O.accumulate(h(40000, 40000, -30000), fp32=True)) == 49984.0    # 50000: a tie, to even
+    assert np.isinf(f16(O.accumulate(h(32768, 32752), fp32=True)))      # 65520 rounds to inf (R4)
+    assert f16(O.accumulate(h(32768, 32736), fp32=True)) == 65504.0      # the largest finite
+    assert f16(O.accumulate(h(2048, 1, 1))) == 2048.0
+    assert f16(O.accumulate(h(2048, 1, 1), fp32=True)) == 2050.0
+    x = np.random.default_rng(2).normal(0, 100, 1000).astype(np.float16).view(np.uint16)
+    assert np.array_equal(O.accumulate([x], fp32=True), x)
+
+
 def test_reduce_spec_examples():
     one = lambda v: np.asarray(v, dtype=np.float16).view(np.uint16)  # noqa: E731
     x = one([1.5, -2.0, 7.0])
