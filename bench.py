@@ -45,6 +45,8 @@ def parse():
                          "replicated = every rank updates the whole vector (the paper's layout); auto = sharded "
                          "when the fused all-reduce is available, else replicated")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
+    ap.add_argument("--accum-fp32", action="store_true",
+                    help="SURVEY Z1 knob (smpu_config.accum_fp32): fp32 accumulator, rn16 of the last sum")
     ap.add_argument("--fuse-final", type=int, choices=[0, 1], default=1,
                     help="W = 1: fuse the last micro-batch's accumulation into Adam (smpu_config.fuse_final, the "
                          "library default; 0 = accumulate, decide, then Adam)")
@@ -401,8 +403,9 @@ def main_ours(args):
                                                              args.optimizer == "auto")
     cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)),
                            allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce], sharded=int(want_shard),
-                           fuse_final=args.fuse_final)
-    fused = world == 1 and args.fuse_final == 1
+                           fuse_final=args.fuse_final, accum_fp32=int(args.accum_fp32))
+    fused = world == 1 and args.fuse_final == 1 and not args.accum_fp32
+    acc32 = args.accum_fp32 and c > 1
     # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
     cfg.growth_interval = 1 << 40
     torch.cuda.synchronize()
@@ -534,7 +537,7 @@ def main_ours(args):
         last = step.result(step.scalars()["attempts"])
         assert last["applied"] == 1 and last["overflow"] == 0, last
         # one pass over the c gradients (+ the accumulator written, then Adam's 28) or, fused, straight into Adam
-        res_bpe = 2 * c + 26 if fused else 2 * c + 2 + 28
+        res_bpe = (10 * c + 22) if acc32 else (2 * c + 26 if fused else 2 * c + 2 + 28)   # fp32 acc.: streaming
         res_bytes = n * res_bpe
         graph_info["resident_microbatches"] = {
             "ms_per_step": ms_res, "value": world * c * n / (ms_res * 1e-3), "unit": UNIT,
@@ -611,19 +614,21 @@ def main_ours(args):
     # algorithmic bytes per launch: K1 first 4 B/elem, K1 add 6, K1s 2, K2 28, K12 (the
     # fused last micro-batch + Adam, W = 1) 30 (28 at c = 1: no accumulator read)
     # (K1s only sweeps when the early decision was undecided; with G_real it returns at once)
-    per_elem = {"k1_first": 4, "k1_add": 6, "k2_adam": 28, "k12_fused": 30 if c > 1 else 28}
+    # with the fp32 accumulator (Z1 knob): first 6 B/elem, add 10, the last micro-batch 8 (rn16 into acc16)
+    shard = sum(h - l for l, h in step.shard_ranges())
     if fused:
-        elems_per_step = {"k1_first": n if c > 1 else 0, "k1_add": max(c - 2, 0) * n, "k2_adam": 0,
-                          "k12_fused": n}
+        step_bytes = {"k1_first": 4 * n if c > 1 else 0, "k1_add": 6 * max(c - 2, 0) * n, "k2_adam": 0,
+                      "k12_fused": (30 if c > 1 else 28) * n}
+    elif acc32:
+        step_bytes = {"k1_first": 6 * n, "k1_add": (10 * (c - 2) + 8) * n, "k2_adam": 28 * shard, "k12_fused": 0}
     else:
-        elems_per_step = {"k1_first": n, "k1_add": (c - 1) * n, "k2_adam": sum(h - l for l, h in step.shard_ranges()),
-                          "k12_fused": 0}
+        step_bytes = {"k1_first": 4 * n, "k1_add": 6 * (c - 1) * n, "k2_adam": 28 * shard, "k12_fused": 0}
     kernels = {}
-    for k, bpe in per_elem.items():
+    for k, per_step in step_bytes.items():
         st = kstat[k]
-        if st["launches"] == 0 or st["ms"] <= 0:
+        if st["launches"] == 0 or st["ms"] <= 0 or per_step == 0:
             continue
-        bytes_total = bpe * elems_per_step[k] * args.steps
+        bytes_total = per_step * args.steps
         kernels[k] = {"launches": st["launches"], "avg_us": 1000 * st["ms"] / st["launches"],
                       "share_of_step": st["ms"] / (ms_calls * args.steps),
                       "algorithmic_bytes_per_launch": bytes_total / st["launches"],
@@ -635,14 +640,14 @@ def main_ours(args):
     roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["achieved_gbs"], "peak": hbm_peak,
             "unit": "GB/s", "frac": kernels[dom]["achieved_gbs"] / hbm_peak, "peak_source": peak_src,
             "traffic": traffic, "frac_of_ncu_dram_peak": kernels[dom]["achieved_gbs"] / ncu_dram_peak}
-    path_bytes = n * ((28 if c == 1 else 6 * c + 22) if fused else 6 * c - 2 + 28)
+    path_bytes = sum(step_bytes.values())
     out = {"metric": METRIC, "value": world * c * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f16+f32", "data": "synthetic",
            "config": {"workload": wl.name, "n_params": n, "n_tensors": len(wl.numel), "update_freq": c,
                       "world": world, "bucket_mib": args.bucket_mib, "n_buckets": nb,
                       "tokens_per_update": int(sum(toks)) * world, "generator": "G_real (SURVEY 8(d.2))",
-                      "parallelism": f"dp{world}", "fuse_final": int(fused),
+                      "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
                       "path_bytes_per_elem": path_bytes / n,
                       "optimizer": "sharded (SURVEY f2)" if (args.sharded and world > 1) else "replicated (paper)", "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"},
            "update_steps_per_s": 1000.0 / ms,

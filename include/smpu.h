@@ -77,6 +77,12 @@ typedef struct {
                                   that becomes current only if R was finite; on a skip w16 is re-cast from the
                                   current theta.  Same arithmetic per element, bitwise (tested); R itself is then
                                   never stored (SMPU_STATE_ACCUM).  0: accumulate, decide, then Adam.            */
+    int32_t accum_fp32;        /* 0 (default, the north star's fp16 accumulation, reading Z1).  1: SURVEY Z1's knob --
+                                  an fp32 accumulator (+4 B per parameter): A32 = fp32(g_1), A32 = fl32(A32 + g_k),
+                                  and the last micro-batch writes the rank's fp16 gradient rn16(A32) into the fp16
+                                  accumulator, from where everything is unchanged (fp16 all-reduce, overflow test,
+                                  Adam).  K1 moves 10 instead of 6 B per element.  fuse_final is then ignored and
+                                  accumulate_many runs one pass per micro-batch.                                    */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */
@@ -169,9 +175,10 @@ smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16);
  * host round trip. */
 smpu_status smpu_loss_scale(const smpu_ctx* ctx, const float** dev_scale);
 
-/* The fp16[n] accumulator itself (device, library-owned, valid until smpu_destroy), for producers that add
- * their weight gradients in place -- e.g. a cuBLAS dW GEMM with beta = 0 for the first micro-batch of an
- * update and beta = 1 after it -- and then declare the micro-batch with micro_grads = NULL below.
+/* The fp16[n] accumulator itself (fp32[n] with accum_fp32; device, library-owned, valid until smpu_destroy),
+ * for producers that add their weight gradients in place -- e.g. a cuBLAS dW GEMM with beta = 0 for the first
+ * micro-batch of an update and beta = 1 after it -- and then declare the micro-batch with
+ * micro_grads = NULL below.
  * The result is the producer's: cuBLAS's fp16 epilogue was measured to compute rn16(rn16(dW) + A), the same
  * two roundings as K1 (reading R1; tests/test_gpu_parity.py), but a GEMM that rounds once would differ. */
 smpu_status smpu_accumulator(const smpu_ctx* ctx, void** dev_acc);

@@ -364,6 +364,94 @@ __global__ void __launch_bounds__(256) k1_scan(const uint16_t* __restrict__ acc,
     if (STATS) publish_max(mx, stat);
 }
 
+// ---------------------------------------------------------------------------------------------- K1 (fp32 acc.)
+// smpu_config.accum_fp32 (SURVEY Z1 knob; oracle.c orc_accumulate32): an fp32 accumulator A32 instead of fp16.
+//   MODE 0  A32 = fp32(g)                       first micro-batch                         6 B/element
+//   MODE 1  A32 = fl32(A32 + fp32(g))           later ones                               10 B/element
+//   MODE 2  acc16 = rn16(fl32(A32 + fp32(g)))   the last one: the rank's fp16 gradient    8 B/element
+//   MODE 3  acc16 = rn16(A32)                   the last one, accumulated in place        6 B/element
+// The fp16 output of modes 2/3 is what K1's last micro-batch would have written (overflow test / max |A| on it);
+// everything downstream (all-reduce, decision, Adam) is unchanged.  16 elements per thread, one-shot grid.
+template <int MODE, bool DETECT, bool STATS>
+__global__ void __launch_bounds__(256, SMPU_K1_MINB) k1_acc32(float* __restrict__ A32, uint16_t* __restrict__ acc16,
+                                                              const uint16_t* __restrict__ g, int64_t lo, int64_t hi,
+                                                              int* __restrict__ flag, uint32_t* __restrict__ stat) {
+    constexpr bool HAS_G = MODE != 3;
+    constexpr bool OUT16 = MODE >= 2;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const uint16_t* gb = g - lo;
+    int64_t vbeg = (lo + 15) & ~(int64_t)15;
+    if (vbeg > hi) vbeg = hi;
+    const bool vec_ok = !HAS_G || ((reinterpret_cast<uintptr_t>(gb + vbeg) & 31) == 0);
+    const int64_t nvec = vec_ok ? (hi - vbeg) / 16 : 0;
+    const int64_t vend = vbeg + nvec * 16;
+    uint32_t bad = 0, mx = 0;
+    if (tid < nvec) {
+        const int64_t i0 = vbeg + tid * 16;
+        V8 gv, a0, a1;
+        if (HAS_G) gv = ld256_ro(gb + i0);
+        if (MODE != 0) {
+            a0 = ld256(A32 + i0);
+            a1 = ld256(A32 + i0 + 8);
+        }
+        if (MODE == 0 || MODE == 1 || MODE == 2) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float2 gf = __half22float2(*reinterpret_cast<const __half2*>(&gv.w[j]));
+                V8& a = j < 4 ? a0 : a1;
+                const int w = 2 * (j & 3);
+                if (MODE == 0) {
+                    a.w[w] = __float_as_uint(gf.x);
+                    a.w[w + 1] = __float_as_uint(gf.y);
+                } else {
+                    a.w[w] = __float_as_uint(__fadd_rn(__uint_as_float(a.w[w]), gf.x));
+                    a.w[w + 1] = __float_as_uint(__fadd_rn(__uint_as_float(a.w[w + 1]), gf.y));
+                }
+            }
+        }
+        if (OUT16) {
+            V8 h;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const V8& a = j < 4 ? a0 : a1;
+                const int w = 2 * (j & 3);
+                __half2 hh = __floats2half2_rn(__uint_as_float(a.w[w]), __uint_as_float(a.w[w + 1]));
+                h.w[j] = *reinterpret_cast<uint32_t*>(&hh);
+                if (DETECT) bad |= nonfinite_bits(h.w[j]);
+                if (STATS) mx = mag_max2(mx, h.w[j]);
+            }
+            st256(acc16 + i0, h);
+        } else {
+            st256(A32 + i0, a0);
+            st256(A32 + i0 + 8, a1);
+        }
+    }
+    auto elem = [&](int64_t i) {
+        float a = MODE == 0 ? 0.0f : A32[i];
+        if (HAS_G) {
+            const float gf = __half2float(__ushort_as_half(gb[i]));
+            a = MODE == 0 ? gf : __fadd_rn(a, gf);
+        }
+        if (OUT16) {
+            const uint16_t x = __half_as_ushort(__float2half_rn(a));
+            if (DETECT && h_nonfinite(x)) bad |= 1u;
+            if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+            acc16[i] = x;
+        } else {
+            A32[i] = a;
+        }
+    };
+    if (vec_ok) {
+        for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
+        for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += nthr) elem(i);
+    }
+    if (DETECT) raise_flag(bad != 0, flag);
+    if (STATS) publish_max(mx, stat);
+}
+
 // ---------------------------------------------------------------------------------------------- K1s
 struct Scalars;
 __device__ __forceinline__ int32_t decision_of(const Scalars* sc);

@@ -5,6 +5,7 @@
 //   theta_b, m_b, v_b fp32[n]                 second bank of them (fuse_final at W = 1: the speculative update)
 //   w16   fp16[n]                             fp16 model weights, re-cast each update
 //   acc   fp16[n]                             accumulator; buckets are views of it
+//   acc32 fp32[n]                             accum_fp32 only: the sums; acc then gets rn16 of the last one
 //   flag int32, stat u32, xs int64[2], DevState, Scalars, loss scale fp32   (device scalars; K0 owns them)
 //   result ring: 64 smpu_step_result in mapped pinned host memory (written by K0).
 //
@@ -66,6 +67,7 @@ struct smpu_ctx {
     float *theta = nullptr, *m = nullptr, *v = nullptr;
     float *theta_b = nullptr, *m_b = nullptr, *v_b = nullptr;   // second bank (fuse_final, world 1)
     bool fused = false;            // fuse_final in effect: the last micro-batch runs k12_fused
+    float* acc32 = nullptr;        // fp32 accumulator (smpu_config.accum_fp32, SURVEY Z1 knob), else null
     bool fused_prepped = false;    // k0_fused_prep enqueued for the open update
     uint16_t *w16 = nullptr, *acc = nullptr;
     int* flag = nullptr;
@@ -410,10 +412,48 @@ smpu_status staged(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, c
     return SMPU_OK;
 }
 
+// fp32-accumulator K1 (k1_acc32) over [lo, hi); g indexed from lo (nullptr in mode 3)
+smpu_status launch_k1_32(smpu_ctx* ctx, int mode, const uint16_t* g, int64_t lo, int64_t hi, bool detect, bool stats,
+                         cudaStream_t s) {
+    if (hi <= lo) return SMPU_OK;
+    const int grid = grid_for((hi - lo + 15) / 16, 0x7fffffff);
+    Timed t(ctx, mode == 0 ? SMPU_K1_FIRST : mode == 3 ? SMPU_K1S : SMPU_K1_ADD, s);
+    float* a = ctx->acc32;
+    uint16_t* h = ctx->acc;
+    int* f = ctx->flag;
+    uint32_t* st = ctx->stat;
+    switch (mode) {
+        case 0: k1_acc32<0, false, false><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st); break;
+        case 1: k1_acc32<1, false, false><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st); break;
+        case 2:
+            if (stats) k1_acc32<2, false, true><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st);
+            else if (detect) k1_acc32<2, true, false><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st);
+            else k1_acc32<2, false, false><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st);
+            break;
+        default:
+            if (stats) k1_acc32<3, false, true><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st);
+            else if (detect) k1_acc32<3, true, false><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st);
+            else k1_acc32<3, false, false><<<grid, 256, 0, s>>>(a, h, g, lo, hi, f, st);
+    }
+    CKL("k1_acc32");
+    return SMPU_OK;
+}
+
 // accumulate src (host or device) into acc[lo, hi); fuse: the last micro-batch at W = 1 with fuse_final, whose
-// elements go straight into Adam (launch_k12) instead
+// elements go straight into Adam (launch_k12) instead; last: this is the update's last micro-batch
 smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int64_t hi, bool first, bool detect,
-                             cudaStream_t s, bool stats = false, bool fuse = false) {
+                             cudaStream_t s, bool stats = false, bool fuse = false, bool last = false) {
+    if (ctx->acc32 && !(src && first && last)) {
+        // fp32 accumulator (c = 1 with a library-read buffer takes the fp16 path below: rn16(fp32(g_1)) = g_1)
+        if (!src) return last ? launch_k1_32(ctx, 3, nullptr, lo, hi, detect, stats, s) : SMPU_OK;
+        const int mode = first ? 0 : last ? 2 : 1;
+        const PtrKind kind = classify(ctx, src);
+        if (kind == PTR_FOREIGN) return set_err(SMPU_EINVAL, "micro-gradients on another device than the ctx's");
+        if (kind == PTR_DEVICE) return launch_k1_32(ctx, mode, src, lo, hi, detect, stats, s);
+        return staged(ctx, src, lo, hi, s, [&](const uint16_t* g, int64_t c0, int64_t c1) {
+            return launch_k1_32(ctx, mode, g, c0, c1, detect, stats, s);
+        });
+    }
     if (fuse) {
         if (!src) return launch_k12(ctx, nullptr, 0, lo, hi, true, s);
         const PtrKind kind = classify(ctx, src);
@@ -612,6 +652,7 @@ void free_ctx(smpu_ctx* c) {
     cudaFree(c->m);
     cudaFree(c->v);
     cudaFree(c->theta_b);
+    cudaFree(c->acc32);
     cudaFree(c->m_b);
     cudaFree(c->v_b);
     if (!c->acc_from_nccl) cudaFree(c->w16);
@@ -681,6 +722,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->allreduce = SMPU_AR_AUTO;
     c->sharded = 0;
     c->fuse_final = 1;
+    c->accum_fp32 = 0;
     return SMPU_OK;
 }
 
@@ -766,7 +808,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMalloc(&ctx->theta, n * 4));
     IK(cudaMalloc(&ctx->m, n * 4));
     IK(cudaMalloc(&ctx->v, n * 4));
-    ctx->fused = world == 1 && cfg->fuse_final != 0;
+    ctx->fused = world == 1 && cfg->fuse_final != 0 && !cfg->accum_fp32;
+    if (cfg->accum_fp32) IK(cudaMalloc(&ctx->acc32, n * 4));
     if (ctx->fused) {
         IK(cudaMalloc(&ctx->theta_b, n * 4));
         IK(cudaMalloc(&ctx->m_b, n * 4));
@@ -863,6 +906,7 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         IK(cudaMemsetAsync(ctx->v_b, 0, n * 4, s0));
     }
     IK(cudaMemsetAsync(ctx->acc, 0, n * 2, s0));
+    if (ctx->acc32) IK(cudaMemsetAsync(ctx->acc32, 0, n * 4, s0));
     IK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), s0));
     IK(cudaMemsetAsync(ctx->stat, 0, sizeof(uint32_t), s0));
     IK(cudaMemsetAsync(ctx->xs, 0, 2 * sizeof(int64_t), s0));
@@ -1004,7 +1048,7 @@ smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_be
 
 smpu_status smpu_accumulator(const smpu_ctx* ctx, void** dev_acc) {
     if (!ctx || !dev_acc) return set_err(SMPU_EINVAL, "null argument");
-    *dev_acc = ctx->acc;
+    *dev_acc = ctx->acc32 ? (void*)ctx->acc32 : (void*)ctx->acc;
     return SMPU_OK;
 }
 
@@ -1066,7 +1110,7 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
     const bool first = ctx->micro == 1;
     const bool multi = last && ctx->world > 1;
     st = accumulate_range(ctx, (const uint16_t*)grads, ctx->bbegin[bucket], ctx->bbegin[bucket + 1], first,
-                          last && ctx->world == 1 && !ctx->fused, s, multi, last && ctx->fused);
+                          last && ctx->world == 1 && !ctx->fused, s, multi, last && ctx->fused, last);
     if (st != SMPU_OK) return st;
     ctx->bucket_done[bucket] = 1;
     if (multi) {
@@ -1110,7 +1154,7 @@ smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, v
     start_micro(ctx, ntokens);
     const bool last = final_micro(ctx);
     st = accumulate_range(ctx, (const uint16_t*)grads, 0, ctx->n, ctx->micro == 1, last && !ctx->fused, s, false,
-                          last && ctx->fused);
+                          last && ctx->fused, last);
     if (st != SMPU_OK) return st;
     return leave_stream(ctx, s);
 }
@@ -1130,6 +1174,13 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const 
         if (!grads[k] || classify(ctx, grads[k]) != PTR_DEVICE)
             return set_err(SMPU_EINVAL, "micro_grads[%d] must be a device buffer", k);
         g[k] = (const uint16_t*)grads[k];
+    }
+    if (ctx->acc32) {     // fp32 accumulator: one pass per micro-batch (the same sums as consecutive calls)
+        for (int k = 0; k < count; ++k) {
+            smpu_status st = smpu_accumulate(ctx, grads[k], ntokens[k], stream);
+            if (st != SMPU_OK) return st;
+        }
+        return SMPU_OK;
     }
     cudaStream_t s = (cudaStream_t)stream;
     smpu_status st = enter_stream(ctx, s);

@@ -19,7 +19,7 @@ def lib_cfg(wl, ocfg: O.Config | None = None, **kw):
     c = smpu.config_default(peak_lr=ocfg.peak_lr, warmup_updates=ocfg.warmup, beta1=ocfg.beta1, beta2=ocfg.beta2,
                             eps=ocfg.eps, init_scale_log2=ocfg.init_scale_log2, min_scale_log2=ocfg.min_scale_log2,
                             max_scale_log2=ocfg.max_scale_log2, growth_interval=ocfg.growth,
-                            update_freq=wl.update_freq)
+                            update_freq=wl.update_freq, accum_fp32=int(ocfg.accum_fp32))
     for k, v in kw.items():
         setattr(c, k, v)
     return c

@@ -39,6 +39,7 @@ def main():
     shard_graph = len(sys.argv) > 4 and sys.argv[4] == "sharded_graph"   # the launch bench.py times at W > 1
     many = len(sys.argv) > 4 and sys.argv[4] == "many"
     external = len(sys.argv) > 4 and sys.argv[4] == "external"
+    acc32 = len(sys.argv) > 4 and sys.argv[4] == "acc32"      # SURVEY Z1 knob: fp32 accumulator, rn16, fp16 AR
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -56,9 +57,10 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     # bucket threshold chosen so buckets split the vector at unaligned boundaries
     ar = {"auto": P.smpu.AR_AUTO, "nccl": P.smpu.AR_NCCL, "fused": P.smpu.AR_FUSED}[impl]
+    ocfg = O.Config(accum_fp32=acc32)
     step = P.UpdateStep(wl.numel, theta0 if rank == 0 else np.zeros_like(theta0),
-                        lib_cfg(wl, bucket_bytes=400_000, allreduce=ar), world=world, rank=rank, nccl_id=obj[0],
-                        device=local)
+                        lib_cfg(wl, ocfg, bucket_bytes=400_000, allreduce=ar), world=world, rank=rank,
+                        nccl_id=obj[0], device=local)
     assert step.n_buckets >= 2
     fused = step.allreduce_impl == P.smpu.AR_FUSED
     if impl == "fused":
@@ -82,7 +84,7 @@ def main():
         if shard_graph:
             sgbufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)]
             shard_step.graph_capture(sgbufs)
-    orc = O.Oracle(theta0) if rank == 0 else None
+    orc = O.Oracle(theta0, ocfg) if rank == 0 else None
     mags = Magnitudes(theta0) if rank == 0 else None
     e = 7
     failures = []
@@ -192,7 +194,7 @@ def main():
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
               f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
               f"{' + sharded optimizer bitwise' if sharded else ''}{' (sharded ctx as CUDA graph)' if shard_graph else ''}{' via accumulate_many' if many else ''}"
-              f"{' with in-place producer accumulation' if external else ''}")
+              f"{' with in-place producer accumulation' if external else ''}{' with the fp32 accumulator' if acc32 else ''}")
 
 
 if __name__ == "__main__":

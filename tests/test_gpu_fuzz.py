@@ -1,6 +1,7 @@
 """Randomised parity (hypothesis, fixed seed): random tensor lists (sizes 1..40k, every class), update_freq 1..5,
 bucket thresholds from a few bytes to 1 MiB, every accumulation entry point (whole / bucket-wise in a random
-order / resident accumulate_many / in-place NULL / CUDA graph), fuse_final on or off, injected non-finites
+order / resident accumulate_many / in-place NULL / CUDA graph), fuse_final on or off, the fp32 accumulator
+(SURVEY Z1 knob) in a quarter of the cases, injected non-finites
 anywhere; the library vs the oracle on decisions (bitwise), the accumulator (bitwise, wherever it holds R) and
 theta/m/v/w16 (tolerance), every update."""
 import numpy as np
@@ -17,8 +18,8 @@ pytestmark = pytest.mark.gpu
 
 
 class _DevView:
-    def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f2", "data": (ptr, False), "version": 3}
+    def __init__(self, ptr, n, typestr="<f2"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
 
 
 @st.composite
@@ -36,7 +37,8 @@ def cases(draw):
     bucket_bytes = draw(st.sampled_from([2, 1000, 16_384, 100_000, 1 << 20]))
     order_seed = draw(st.integers(0, 1000))
     fuse = draw(st.booleans())
-    return tensors, c, inj, mode, bucket_bytes, order_seed, fuse
+    acc32 = draw(st.integers(0, 3)) == 0          # the Z1 fp32-accumulator knob in a quarter of the cases
+    return tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32
 
 
 @seed(20261018)
@@ -45,18 +47,21 @@ def cases(draw):
 def test_fuzz_against_oracle(case):
     import torch
     import paper_1806_00187_b200 as P
-    tensors, c, inj, mode, bucket_bytes, order_seed, fuse = case
+    tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32 = case
     wl = models.Workload("fuzz", tensors, 1, c, injections=inj)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
-    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=bucket_bytes, fuse_final=int(fuse)))
-    orc = O.Oracle(theta0)
+    ocfg = O.Config(accum_fp32=acc32)
+    fuse = fuse and not acc32                       # the library ignores fuse_final with the fp32 accumulator
+    step = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, ocfg, bucket_bytes=bucket_bytes, fuse_final=int(fuse)))
+    orc = O.Oracle(theta0, ocfg)
     mags = Magnitudes(theta0)
     rng = np.random.default_rng(order_seed)
     bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)] if mode == "graph" else None
     if mode == "graph":
         step.graph_capture(bufs)
-    acc = torch.as_tensor(_DevView(step.accumulator_ptr(), lay.n), device="cuda") if mode == "inplace" else None
+    acc = torch.as_tensor(_DevView(step.accumulator_ptr(), lay.n, "<f4" if acc32 else "<f2"), device="cuda") \
+        if mode == "inplace" else None
     for u in range(1, 4):
         e = orc.e
         grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in range(1, c + 1)]
@@ -77,6 +82,8 @@ def test_fuzz_against_oracle(case):
                     step.accumulate(dev[k], toks[k])
                 elif mode == "inplace":
                     g = dev[k].view(torch.float16)
+                    if acc32:
+                        g = g.float()                   # binary32 round-to-nearest adds, as the oracle's variant
                     acc.copy_(g) if k == 0 else acc.add_(g)
                     step.accumulate(None, toks[k])
                 else:

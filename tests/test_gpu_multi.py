@@ -15,11 +15,11 @@ def _ngpu():
 
 
 def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False, many=False,
-         external=False):
+         external=False, acc32=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
            str(updates), impl] + (["graph"] if graph else []) + ([sharded if isinstance(sharded, str) else "sharded"] if sharded else []) + \
-          (["many"] if many else []) + (["external"] if external else [])
+          (["many"] if many else []) + (["external"] if external else []) + (["acc32"] if acc32 else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
@@ -53,6 +53,14 @@ def test_world2_accumulate_many_final_microbatch():
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, "real", port=29539, impl="fused", many=True)
+
+
+def test_world2_accum_fp32():
+    """SURVEY Z1 knob at W = 2: per-rank fp32 sums, rn16, the fused fp16 all-reduce; R bitwise the oracle's
+    binary32 variant, decisions bitwise, replicas identical."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "real", port=29567, impl="fused", acc32=True)
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -141,6 +141,64 @@ def test_two_x_lr_and_update_freq_1(P):
     run_pair(P, wl, 4, ocfg=ocfg, rtol_last=1e-5)
 
 
+@pytest.mark.parametrize("mode,host", [("whole", None), ("bucket", None), ("whole", "pinned")])
+def test_accum_fp32_knob(P, mode, host):
+    """SURVEY Z1 knob (smpu_config.accum_fp32): fp32 sums, rn16 of the last one, against the oracle's binary32
+    variant -- the reduced gradient bitwise, decisions bitwise, state within tolerance -- through an overflow that
+    only the fp16 accumulator would raise, one that both raise, and a NaN."""
+    tensors = [("a", 17, 1), ("b", 100_003, 0), ("c", 65_536, 2), ("d", 9, 1)]
+    inj = [dict(u=2, kind="ACC_OVF", r=0, i=70_000), dict(u=4, kind="NAN", r=0, k=2, i=100_019),
+           dict(u=5, kind="INF", r=0, k=1, i=3)]
+    wl = models.Workload("acc32", tensors, 1, 4, injections=inj)
+    run_pair(P, wl, 6, ocfg=O.Config(accum_fp32=True), cfg_kw=dict(bucket_bytes=64 * 1024), mode=mode,
+             host_inputs=host, rtol_last=1e-5)
+
+
+def test_accum_fp32_many_and_inplace(P):
+    """accum_fp32 through accumulate_many (one pass per micro-batch) and an in-place producer adding into the fp32
+    accumulator (torch fp32 adds are binary32 round-to-nearest): bitwise the streaming fp32 path."""
+    import torch
+    tensors = [("a", 17, 1), ("b", 100_003, 0), ("c", 65_536, 2)]
+    wl = models.Workload("acc32m", tensors, 1, 5, injections=[dict(u=3, kind="NAN", r=0, k=4, i=100_010)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    ocfg = O.Config(accum_fp32=True)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, ocfg))
+    b = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, ocfg))
+    x = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, ocfg, bucket_bytes=100_000))
+    acc = torch.as_tensor(_DevView(x.accumulator_ptr(), lay.n, "<f4"), device="cuda")
+    orc = O.Oracle(theta0, ocfg)
+    for u in range(1, 5):
+        e = orc.e
+        grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in range(1, 6)]
+        toks = [synth.ntokens(wl, u, 0, k) for k in range(1, 6)]
+        ores = orc.update([grads], [toks])
+        dev = [h2t(g) for g in grads]
+        for k in range(5):
+            a.accumulate(dev[k], toks[k])
+        b.accumulate_many(dev[:3], toks[:3])
+        b.accumulate_many(dev[3:], toks[3:])
+        for k in range(5):
+            g32 = dev[k].view(torch.float16).float()
+            acc.copy_(g32) if k == 0 else acc.add_(g32)
+            if k < 4:
+                x.accumulate(None, toks[k])
+            else:
+                x.micro_begin(toks[k])
+                for bk in reversed(range(x.n_buckets)):
+                    x.accumulate_bucket(bk, None)
+        ra, rb, rx = a.step(), b.step(), x.step()
+        assert decisions(ra) == decisions(rb) == decisions(rx) == oracle_decisions(ores), u
+        R = ores["R"]
+        nan = np.isnan(R.view(np.float16))
+        for st in (a, b, x):
+            got = st.get_state(P.smpu.STATE_ACCUM)
+            assert np.array_equal(np.isnan(got.view(np.float16)), nan) and np.array_equal(got[~nan], R[~nan]), u
+        for w in (0, 1, 2, 3, 5):
+            sa = a.get_state(w)
+            assert np.array_equal(sa, b.get_state(w)) and np.array_equal(sa, x.get_state(w)), (u, w)
+
+
 def test_bucket_size_invariance(P):
     # buckets change timing, never values (P:209-212): final state bitwise equal for any bucket size
     import torch
