@@ -166,8 +166,11 @@ smpu_status smpu_allreduce_impl(const smpu_ctx* ctx, int* impl);
 /* Bucket boundaries chosen at init (same as smpu_plan_buckets with cfg->bucket_bytes). */
 smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_begin /* or NULL */);
 
-/* Device fp16[n] weights (library-owned, valid until smpu_destroy).  Rewritten only by smpu_step,
- * in stream order on the stream passed to it. */
+/* Device fp16[n] weights (library-owned, valid until smpu_destroy).  Rewritten by smpu_step, in stream order on
+ * the stream passed to it -- and, with fuse_final at world 1, already by the last micro-batch's accumulate call
+ * (or each bucket's, in stream order on its stream: a bucket is handed over once its gradients are done, so the
+ * backward no longer reads those weights); a skipped update restores them in smpu_step.  Read them for the next
+ * forward after smpu_step. */
 smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16);
 
 /* Device fp32 scalar holding the current loss scale 2^e ("we scale the loss right after the forward
