@@ -113,3 +113,25 @@ def test_kernel_ids_match_header(P):
     for name, k in ids.items():
         if name != "N_KERNELS":
             assert getattr(P.smpu, name) == k, name
+
+
+def test_struct_layouts_match_header(P, tmp_path):
+    """The ctypes mirrors of smpu_config / smpu_step_result have the C layout: offsets and sizes printed by a C
+    program compiled against include/smpu.h (a field added on one side only would shift every later field)."""
+    import subprocess
+    src = tmp_path / "layout.c"
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "smpu.h"', "int main(void) {"]
+    for cname, py in (("smpu_config", P.smpu.Config), ("smpu_step_result", P.smpu.StepResult)):
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], check=True, capture_output=True,
+                                                        text=True).stdout.splitlines())
+    for cname, py in (("smpu_config", P.smpu.Config), ("smpu_step_result", P.smpu.StepResult)):
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, f"{cname}.{f}"
