@@ -135,3 +135,18 @@ def test_struct_layouts_match_header(P, tmp_path):
         assert int(got[cname]) == ctypes.sizeof(py), cname
         for f, _ in py._fields_:
             assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, f"{cname}.{f}"
+
+
+def test_missing_library_is_an_import_error(tmp_path):
+    """No silent fallback: the package without its built libsmpu.so refuses to import."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_1806_00187_b200"
+    pkg.mkdir()
+    for f in os.listdir(os.path.join(ROOT, "paper_1806_00187_b200")):
+        if f.endswith(".py"):
+            shutil.copy(os.path.join(ROOT, "paper_1806_00187_b200", f), pkg / f)
+    r = subprocess.run([sys.executable, "-c", "import paper_1806_00187_b200"], cwd=tmp_path, capture_output=True,
+                       text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr
