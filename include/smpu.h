@@ -83,6 +83,10 @@ typedef struct {
                                   accumulator, from where everything is unchanged (fp16 all-reduce, overflow test,
                                   Adam).  K1 moves 10 instead of 6 B per element.  fuse_final is then ignored and
                                   accumulate_many runs one pass per micro-batch.                                    */
+    int32_t split_tensors;     /* 0 (default): the paper's plan, whole tensors per bucket (R17).  1: fixed
+                                  buckets of bucket_bytes (rounded up to 128 elements) cut wherever they fall, so a
+                                  tensor may span buckets (smpu_tensor_ready then counts it in each).  Buckets
+                                  change timing, never values.                                        */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */
@@ -163,7 +167,7 @@ smpu_status smpu_shard_ranges(const smpu_ctx* ctx, int64_t* ranges, int cap, int
 /* Which bucket all-reduce this ctx runs (SMPU_AR_NCCL or SMPU_AR_FUSED; 0 at world == 1). */
 smpu_status smpu_allreduce_impl(const smpu_ctx* ctx, int* impl);
 
-/* Bucket boundaries chosen at init (same as smpu_plan_buckets with cfg->bucket_bytes). */
+/* Bucket boundaries chosen at init (same as smpu_plan_buckets with cfg->bucket_bytes unless split_tensors). */
 smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_begin /* or NULL */);
 
 /* Device fp16[n] weights (library-owned, valid until smpu_destroy).  Rewritten by smpu_step, in stream order on

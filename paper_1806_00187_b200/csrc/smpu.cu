@@ -58,8 +58,9 @@ struct smpu_ctx {
     int world = 1, rank = 0, dev = 0;
     int64_t n = 0;
     std::vector<int64_t> bbegin;   // bucket element offsets, size nb+1
-    std::vector<int> tensor_bucket;                 // bucket of each tensor (plan order)
-    std::vector<int> bucket_tensors;                // tensors per bucket
+    std::vector<int> tensor_bucket;                 // first bucket of each tensor (plan order)
+    std::vector<int> tensor_bucket_last;            // last bucket of each tensor (> first only with split_tensors)
+    std::vector<int> bucket_tensors;                // tensors overlapping each bucket
     std::vector<int> bucket_tensors_left;           // of the open micro-batch (smpu_tensor_ready)
     std::vector<char> tensor_seen;                  // of the open micro-batch
     int nb = 0;
@@ -609,10 +610,24 @@ smpu_status issue_decision(smpu_ctx* ctx) {
     return SMPU_OK;
 }
 
-smpu_status plan(const int64_t* numel, int n_tensors, int64_t bucket_bytes, std::vector<int64_t>& out) {
+// split = 0: the paper's plan, whole tensors, a bucket closes once it reaches bucket_bytes (R17).
+// split = 1 (smpu_config.split_tensors): fixed-size buckets of bucket_bytes rounded up to 128 elements (256 B),
+// cut wherever they fall -- tensors may span buckets; the remainder is the last bucket.
+smpu_status plan(const int64_t* numel, int n_tensors, int64_t bucket_bytes, std::vector<int64_t>& out,
+                 bool split = false) {
     out.clear();
     out.push_back(0);
     int64_t off = 0, cur = 0;
+    if (split) {
+        for (int j = 0; j < n_tensors; ++j) {
+            if (numel[j] <= 0) return set_err(SMPU_EINVAL, "numel[%d] = %lld must be > 0", j, (long long)numel[j]);
+            off += numel[j];
+        }
+        const int64_t per = ((bucket_bytes / 2 + 127) / 128) * 128;
+        for (int64_t b = per; b < off; b += per) out.push_back(b);
+        out.push_back(off);
+        return SMPU_OK;
+    }
     for (int j = 0; j < n_tensors; ++j) {
         if (numel[j] <= 0) return set_err(SMPU_EINVAL, "numel[%d] = %lld must be > 0", j, (long long)numel[j]);
         off += numel[j];
@@ -723,6 +738,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->sharded = 0;
     c->fuse_final = 1;
     c->accum_fp32 = 0;
+    c->split_tensors = 0;
     return SMPU_OK;
 }
 
@@ -761,7 +777,7 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     ctx->world = world;
     ctx->rank = rank;
     ctx->dev = cuda_device;
-    s = plan(numel, n_tensors, cfg->bucket_bytes, ctx->bbegin);
+    s = plan(numel, n_tensors, cfg->bucket_bytes, ctx->bbegin, cfg->split_tensors != 0);
     if (s != SMPU_OK) {
         delete ctx;
         return s;
@@ -769,13 +785,17 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     ctx->nb = (int)ctx->bbegin.size() - 1;
     {
         ctx->tensor_bucket.resize(n_tensors);
+        ctx->tensor_bucket_last.resize(n_tensors);
         ctx->bucket_tensors.assign(ctx->nb, 0);
         int64_t off = 0;
         int b = 0;
         for (int j = 0; j < n_tensors; ++j) {
             while (b + 1 < ctx->nb && off >= ctx->bbegin[b + 1]) ++b;
+            int e = b;
+            while (e + 1 < ctx->nb && off + numel[j] > ctx->bbegin[e + 1]) ++e;
             ctx->tensor_bucket[j] = b;
-            ctx->bucket_tensors[b]++;
+            ctx->tensor_bucket_last[j] = e;
+            for (int k = b; k <= e; ++k) ctx->bucket_tensors[k]++;
             off += numel[j];
         }
         ctx->bucket_tensors_left = ctx->bucket_tensors;
@@ -1086,12 +1106,17 @@ smpu_status smpu_tensor_ready(smpu_ctx* ctx, int tensor, void* stream) {
     if (tensor < 0 || tensor >= (int)ctx->tensor_bucket.size())
         return set_err(SMPU_EINVAL, "tensor %d out of [0, %d)", tensor, (int)ctx->tensor_bucket.size());
     if (ctx->tensor_seen[tensor]) return set_err(SMPU_ESTATE, "tensor %d already ready in this micro-batch", tensor);
-    const int b = ctx->tensor_bucket[tensor];
-    if (ctx->bucket_done[b]) return set_err(SMPU_ESTATE, "bucket %d of tensor %d was already given", b, tensor);
+    const int b0 = ctx->tensor_bucket[tensor], b1 = ctx->tensor_bucket_last[tensor];
+    for (int b = b0; b <= b1; ++b)
+        if (ctx->bucket_done[b]) return set_err(SMPU_ESTATE, "bucket %d of tensor %d was already given", b, tensor);
     ctx->tensor_seen[tensor] = 1;
     // "when the gradient computation for a layer finishes, we add the result to a synchronization buffer; as
     // soon as the size of the buffer reaches a predefined threshold we synchronize"
-    if (--ctx->bucket_tensors_left[b] == 0) return smpu_accumulate_bucket(ctx, b, nullptr, stream);
+    for (int b = b0; b <= b1; ++b)
+        if (--ctx->bucket_tensors_left[b] == 0) {
+            smpu_status st = smpu_accumulate_bucket(ctx, b, nullptr, stream);
+            if (st != SMPU_OK) return st;
+        }
     return SMPU_OK;
 }
 

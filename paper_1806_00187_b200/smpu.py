@@ -39,7 +39,7 @@ class Config(ctypes.Structure):
                 ("min_scale_log2", ctypes.c_int32), ("max_scale_log2", ctypes.c_int32),
                 ("growth_interval", ctypes.c_int64), ("update_freq", ctypes.c_int32),
                 ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32), ("sharded", ctypes.c_int32),
-                ("fuse_final", ctypes.c_int32), ("accum_fp32", ctypes.c_int32)]
+                ("fuse_final", ctypes.c_int32), ("accum_fp32", ctypes.c_int32), ("split_tensors", ctypes.c_int32)]
 
 
 class StepResult(ctypes.Structure):

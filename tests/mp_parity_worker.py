@@ -40,6 +40,7 @@ def main():
     many = len(sys.argv) > 4 and sys.argv[4] == "many"
     external = len(sys.argv) > 4 and sys.argv[4] == "external"
     acc32 = len(sys.argv) > 4 and sys.argv[4] == "acc32"      # SURVEY Z1 knob: fp32 accumulator, rn16, fp16 AR
+    split = len(sys.argv) > 4 and sys.argv[4] == "split"      # smpu_config.split_tensors: buckets cut tensors
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -59,7 +60,8 @@ def main():
     ar = {"auto": P.smpu.AR_AUTO, "nccl": P.smpu.AR_NCCL, "fused": P.smpu.AR_FUSED}[impl]
     ocfg = O.Config(accum_fp32=acc32)
     step = P.UpdateStep(wl.numel, theta0 if rank == 0 else np.zeros_like(theta0),
-                        lib_cfg(wl, ocfg, bucket_bytes=400_000, allreduce=ar), world=world, rank=rank,
+                        lib_cfg(wl, ocfg, bucket_bytes=400_000, allreduce=ar, split_tensors=int(split)), world=world,
+                        rank=rank,
                         nccl_id=obj[0], device=local)
     assert step.n_buckets >= 2
     fused = step.allreduce_impl == P.smpu.AR_FUSED
@@ -194,7 +196,7 @@ def main():
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
               f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
               f"{' + sharded optimizer bitwise' if sharded else ''}{' (sharded ctx as CUDA graph)' if shard_graph else ''}{' via accumulate_many' if many else ''}"
-              f"{' with in-place producer accumulation' if external else ''}{' with the fp32 accumulator' if acc32 else ''}")
+              f"{' with in-place producer accumulation' if external else ''}{' with the fp32 accumulator' if acc32 else ''}{' with split-tensor buckets' if split else ''}")
 
 
 if __name__ == "__main__":

@@ -15,11 +15,12 @@ def _ngpu():
 
 
 def _run(world, family, updates=8, port=29531, impl="auto", graph=False, sharded=False, many=False,
-         external=False, acc32=False):
+         external=False, acc32=False, split=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/mp_parity_worker.py", family,
            str(updates), impl] + (["graph"] if graph else []) + ([sharded if isinstance(sharded, str) else "sharded"] if sharded else []) + \
-          (["many"] if many else []) + (["external"] if external else []) + (["acc32"] if acc32 else [])
+          (["many"] if many else []) + (["external"] if external else []) + (["acc32"] if acc32 else []) + \
+          (["split"] if split else [])
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(p.stdout[-4000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
@@ -53,6 +54,13 @@ def test_world2_accumulate_many_final_microbatch():
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, "real", port=29539, impl="fused", many=True)
+
+
+def test_world2_split_tensor_buckets():
+    """split_tensors at W = 2: buckets cut through tensors, fused all-reduce per bucket; bitwise the oracle."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "real", port=29571, impl="fused", split=True)
 
 
 def test_world2_accum_fp32():

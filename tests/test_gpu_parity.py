@@ -199,6 +199,45 @@ def test_accum_fp32_many_and_inplace(P):
             assert np.array_equal(sa, b.get_state(w)) and np.array_equal(sa, x.get_state(w)), (u, w)
 
 
+def test_split_tensor_buckets(P):
+    """smpu_config.split_tensors: fixed 128-element-aligned buckets cut through tensors.  Whole, bucket-wise (random
+    order) and in-place per-tensor-hook micro-batches give the default plan's bits (buckets change timing, never
+    values); a tensor spanning several buckets is counted in each by smpu_tensor_ready."""
+    import torch
+    tensors = [("a", 17, 1), ("b", 300_001, 0), ("c", 65_536, 2), ("d", 9, 1)]
+    wl = models.Workload("split", tensors, 1, 3, injections=[dict(u=2, kind="NAN", r=0, k=3, i=150_000)])
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    x = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, bucket_bytes=100_000, split_tensors=1))
+    per = 50_048
+    assert x.bucket_begin.tolist() == list(range(0, lay.n, per)) + [lay.n]
+    acc = torch.as_tensor(_DevView(x.accumulator_ptr(), lay.n), device="cuda")
+    orc = O.Oracle(theta0)
+    rng = np.random.default_rng(5)
+    for u in range(1, 5):
+        e = orc.e
+        grads = [synth.micro_grad_cpu(wl, lay, u, 0, k, e) for k in (1, 2, 3)]
+        toks = [synth.ntokens(wl, u, 0, k) for k in (1, 2, 3)]
+        ores = orc.update([grads], [toks])
+        dev = [h2t(g) for g in grads]
+        for k in range(3):
+            a.accumulate(dev[k], toks[k])
+        x.accumulate(dev[0], toks[0])
+        x.micro_begin(toks[1])
+        bb = x.bucket_begin
+        for b in rng.permutation(x.n_buckets):
+            x.accumulate_bucket(int(b), dev[1][bb[b]:bb[b + 1]])
+        acc.add_(dev[2].view(torch.float16))            # the in-place producer's last micro-batch
+        x.micro_begin(toks[2])
+        for j in rng.permutation(len(tensors)):
+            x.tensor_ready(int(j))
+        ra, rx = a.step(), x.step()
+        assert decisions(ra) == decisions(rx) == oracle_decisions(ores), u
+        for w in (0, 1, 2, 3, 5):
+            assert np.array_equal(a.get_state(w), x.get_state(w)), (u, w)
+
+
 def test_bucket_size_invariance(P):
     # buckets change timing, never values (P:209-212): final state bitwise equal for any bucket size
     import torch
