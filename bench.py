@@ -45,6 +45,8 @@ def parse():
                          "replicated = every rank updates the whole vector (the paper's layout); auto = sharded "
                          "when the fused all-reduce is available, else replicated")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
+    ap.add_argument("--generator", choices=["real", "exact", "zero"], default="real",
+                    help="input family (SURVEY 8(d.2)); the performance-independence check times all three")
     ap.add_argument("--accum-fp32", action="store_true",
                     help="SURVEY Z1 knob (smpu_config.accum_fp32): fp32 accumulator, rn16 of the last sum")
     ap.add_argument("--fuse-final", type=int, choices=[0, 1], default=1,
@@ -382,6 +384,7 @@ def main_ours(args):
     from paper_1806_00187_b200 import smpu
 
     wl = workload(args.config, world, args.update_freq)
+    wl.family = args.generator
     lay = synth.Layout(wl)
     c, n = wl.update_freq, lay.n
     nccl_id = None
@@ -646,7 +649,7 @@ def main_ours(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "f16+f32", "data": "synthetic",
            "config": {"workload": wl.name, "n_params": n, "n_tensors": len(wl.numel), "update_freq": c,
                       "world": world, "bucket_mib": args.bucket_mib, "n_buckets": nb,
-                      "tokens_per_update": int(sum(toks)) * world, "generator": "G_real (SURVEY 8(d.2))",
+                      "tokens_per_update": int(sum(toks)) * world, "generator": {"real": "G_real", "exact": "G_exact", "zero": "zeros"}[args.generator] + " (SURVEY 8(d.2))",
                       "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
                       "path_bytes_per_elem": path_bytes / n,
                       "optimizer": "sharded (SURVEY f2)" if (args.sharded and world > 1) else "replicated (paper)", "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"},
