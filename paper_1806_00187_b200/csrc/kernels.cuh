@@ -10,6 +10,9 @@
 //   K2   adam         fused unscale + normalise by N + Adam (fp32 master) + fp16 re-cast, per bucket right
 //                     behind that bucket's all-reduce (W > 1) or whole (W = 1); every CTA exits before any
 //                     store when K0 decided to skip.
+//   K12  fused        W = 1 (fuse_final): the last micro-batch's K1 add fused into K2, computed speculatively into
+//                     a second bank of theta/m/v (k12_fused, k12_fused_many); kc_restore re-casts w16 on a skip.
+//   K1 fp32           accum_fp32 (SURVEY Z1 knob): fp32 sums, rn16 of the last one into the fp16 accumulator.
 //   Kc   cast         w16 = rn16(theta) (init / set_state only).
 //
 // All of them are HBM-streaming: 256-bit (v8.b32) global accesses (sm_100a LDG/STG.256), L1 no-allocate,
