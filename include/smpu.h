@@ -146,6 +146,14 @@ smpu_status smpu_unique_id(void* out, int64_t bytes);
 smpu_status smpu_plan_buckets(const int64_t* numel, int n_tensors, int64_t bucket_bytes, int* n_buckets,
                               int64_t* bucket_begin);
 
+/* Host-only shard plan of the sharded layout: the element ranges whose theta/m/v rank `rank` of
+ * `world` updates, for the buckets bucket_begin[0..n_buckets] (as smpu_plan_buckets / smpu_buckets give them):
+ * per bucket, 8-element units from its first multiple of 8, ceil(units / world) consecutive units per rank, and
+ * the bucket's unaligned head and tail to rank 0 -- the split the device reduce-scatter makes.  Same output
+ * convention as smpu_shard_ranges (ranges host, capacity 2*cap; NULL to query).  Needs no GPU. */
+smpu_status smpu_plan_shards(const int64_t* bucket_begin, int n_buckets, int world, int rank, int64_t* ranges,
+                             int cap, int* count);
+
 /* Create a ctx on CUDA device `cuda_device`.
  *   cfg          host; copied.
  *   world, rank  0 <= rank < world.  world > 1 needs nccl_id (host, 128 B, identical on every rank) and

@@ -641,6 +641,23 @@ smpu_status plan(const int64_t* numel, int n_tensors, int64_t bucket_bytes, std:
     return SMPU_OK;
 }
 
+// This rank's element ranges of bucket [lo, hi) in the sharded layout -- the split k_rs_lsa makes on the device:
+// 8-element units from the first multiple of 8, ceil(units / W) per rank; rank 0 also owns the unaligned head and
+// tail.  Host-only (smpu_plan_shards exports it for tests).
+void shard_of_bucket(int64_t lo, int64_t hi, int world, int rank, std::vector<std::pair<int64_t, int64_t>>& out) {
+    const int64_t v0 = (lo + 7) & ~(int64_t)7, v1 = hi & ~(int64_t)7;
+    const int64_t units = v1 > v0 ? (v1 - v0) / 8 : 0, per = (units + world - 1) / world;
+    int64_t u_lo = rank * per, u_hi = u_lo + per;
+    if (u_lo > units) u_lo = units;
+    if (u_hi > units) u_hi = units;
+    out.push_back({v0 + u_lo * 8, v0 + u_hi * 8});
+    if (rank == 0) {
+        const int64_t head_end = v0 < hi ? v0 : hi;
+        out.push_back({lo, head_end});
+        out.push_back({v1 > head_end ? v1 : head_end, hi});
+    }
+}
+
 smpu_status check_cfg(const smpu_config* c) {
     if (!c) return set_err(SMPU_EINVAL, "null cfg");
     if (c->update_freq < 1) return set_err(SMPU_EINVAL, "update_freq must be >= 1");
@@ -759,6 +776,29 @@ smpu_status smpu_plan_buckets(const int64_t* numel, int n_tensors, int64_t bucke
     if (s != SMPU_OK) return s;
     *n_buckets = (int)b.size() - 1;
     if (bucket_begin) memcpy(bucket_begin, b.data(), b.size() * sizeof(int64_t));
+    return SMPU_OK;
+}
+
+smpu_status smpu_plan_shards(const int64_t* bucket_begin, int n_buckets, int world, int rank, int64_t* ranges,
+                             int cap, int* count) {
+    if (!bucket_begin || n_buckets < 1 || world < 1 || rank < 0 || rank >= world || !count)
+        return set_err(SMPU_EINVAL, "bad arguments");
+    for (int b = 0; b < n_buckets; ++b)
+        if (bucket_begin[b + 1] < bucket_begin[b]) return set_err(SMPU_EINVAL, "bucket_begin must not decrease");
+    int k = 0;
+    for (int b = 0; b < n_buckets; ++b) {
+        std::vector<std::pair<int64_t, int64_t>> v;
+        shard_of_bucket(bucket_begin[b], bucket_begin[b + 1], world, rank, v);
+        for (auto& rg : v) {
+            if (rg.second <= rg.first) continue;
+            if (ranges && k < cap) {
+                ranges[2 * k] = rg.first;
+                ranges[2 * k + 1] = rg.second;
+            }
+            ++k;
+        }
+    }
+    *count = k;
     return SMPU_OK;
 }
 
@@ -995,20 +1035,8 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                 // the same shard split as k_rs_lsa: 8-element units, ceil(units / W) per rank, rank 0 also
                 // owns the bucket's unaligned head and tail
                 ctx->shard.resize(ctx->nb);
-                for (int b = 0; b < ctx->nb; ++b) {
-                    const int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
-                    const int64_t v0 = (lo + 7) & ~(int64_t)7, v1 = hi & ~(int64_t)7;
-                    const int64_t units = v1 > v0 ? (v1 - v0) / 8 : 0, per = (units + world - 1) / world;
-                    int64_t u_lo = rank * per, u_hi = u_lo + per;
-                    if (u_lo > units) u_lo = units;
-                    if (u_hi > units) u_hi = units;
-                    ctx->shard[b].push_back({v0 + u_lo * 8, v0 + u_hi * 8});
-                    if (rank == 0) {
-                        const int64_t head_end = v0 < hi ? v0 : hi;
-                        ctx->shard[b].push_back({lo, head_end});
-                        ctx->shard[b].push_back({v1 > head_end ? v1 : head_end, hi});
-                    }
-                }
+                for (int b = 0; b < ctx->nb; ++b)
+                    shard_of_bucket(ctx->bbegin[b], ctx->bbegin[b + 1], world, rank, ctx->shard[b]);
             }
             if (cfg->sharded && !ctx->sharded)
                 return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce (unavailable)"));

@@ -53,7 +53,7 @@ class StepResult(ctypes.Structure):
 
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
-           "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_allreduce_impl", "smpu_buckets",
+           "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_plan_shards", "smpu_allreduce_impl", "smpu_buckets",
            "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate", "smpu_accumulate_many", "smpu_micro_begin",
            "smpu_accumulate_bucket", "smpu_tensor_ready", "smpu_step", "smpu_allreduce_accumulator", "smpu_graph_capture",
            "smpu_graph_launch", "smpu_result", "smpu_get_master", "smpu_get_state", "smpu_set_state",
@@ -80,6 +80,7 @@ def lib():
             "smpu_num_params": ([p, P(ctypes.c_int64)], st),
             "smpu_allreduce_impl": ([p, P(ctypes.c_int)], st),
             "smpu_shard_ranges": ([p, p, i32, P(ctypes.c_int)], st),
+            "smpu_plan_shards": ([p, i32, i32, i32, p, i32, P(ctypes.c_int)], st),
             "smpu_buckets": ([p, P(ctypes.c_int), p], st),
             "smpu_weights_fp16": ([p, P(p)], st),
             "smpu_accumulator": ([p, P(p)], st),
@@ -172,6 +173,16 @@ def plan_buckets(numel, bucket_bytes: int) -> np.ndarray:
     out = np.zeros(numel.size + 1, dtype=np.int64)
     _check(lib().smpu_plan_buckets(_ptr(numel), numel.size, bucket_bytes, ctypes.byref(nb), _ptr(out)))
     return out[: nb.value + 1].copy()
+
+
+def plan_shards(bucket_begin, world: int, rank: int):
+    """Host-only: [(lo, hi)] element ranges rank `rank` of `world` updates in the sharded layout."""
+    bb = np.ascontiguousarray(bucket_begin, dtype=np.int64)
+    cnt = ctypes.c_int()
+    _check(lib().smpu_plan_shards(_ptr(bb), bb.size - 1, world, rank, None, 0, ctypes.byref(cnt)))
+    buf = np.zeros(2 * max(cnt.value, 1), dtype=np.int64)
+    _check(lib().smpu_plan_shards(_ptr(bb), bb.size - 1, world, rank, _ptr(buf), cnt.value, ctypes.byref(cnt)))
+    return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(cnt.value)]
 
 
 class UpdateStep:

@@ -150,3 +150,32 @@ def test_missing_library_is_an_import_error(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_1806_00187_b200"], cwd=tmp_path, capture_output=True,
                        text=True)
     assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 5, 6, 7, 8])
+def test_shard_plan_partitions_every_bucket(P, world):
+    """Host logic of the sharded layout at every world size the peer kernels take, W = 8 included
+    (gpurun grants at most 4 GPUs): the ranks' ranges cover every element exactly once, stay inside their
+    bucket, are 8-element aligned except rank 0's bucket heads / tails, and split each bucket's units evenly."""
+    rng = np.random.default_rng(world)
+    for trial in range(20):
+        numel = rng.integers(1, 5000, rng.integers(1, 12))
+        bb = P.plan_buckets(numel, int(rng.choice([2, 100, 3000, 20000])))
+        n = int(bb[-1])
+        mark = np.zeros(n, np.int32)
+        for r in range(world):
+            for lo, hi in P.smpu.plan_shards(bb, world, r):
+                assert 0 <= lo < hi <= n
+                b = int(np.searchsorted(bb, lo, side="right")) - 1
+                assert hi <= bb[b + 1], "a range crosses a bucket boundary"
+                if r > 0:
+                    assert lo % 8 == 0 and hi % 8 == 0
+                mark[lo:hi] += 1
+        assert (mark == 1).all(), (trial, world)
+        for b in range(len(bb) - 1):                        # the aligned units are split evenly
+            v0, v1 = (bb[b] + 7) // 8 * 8, bb[b + 1] // 8 * 8
+            units = max(v1 - v0, 0) // 8
+            per = -(-units // world)
+            sizes = [sum(min(h, v1) - max(l, v0) for l, h in P.smpu.plan_shards(bb[b:b + 2], world, r)
+                         if min(h, v1) > max(l, v0)) // 8 for r in range(world)]
+            assert sum(sizes) == units and max(sizes, default=0) <= per
