@@ -254,7 +254,7 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out);
 smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, int count, int flags);
 smpu_status smpu_graph_launch(smpu_ctx* ctx, const int64_t* ntokens, int count, void* stream);
 
-/* The bucketed all-reduce alone (a collective primitive and a benchmark handle): sums the accumulator over
+/* The bucketed all-reduce alone (a collective primitive and a benchmark handle): sums the fp16 accumulator over
  * all ranks in place, bucket by bucket in canonical order, with this ctx's implementation (fused deterministic
  * or NCCL), stream-ordered on `stream`.  Collective; between updates only (ESTATE inside one); no-op at
  * world == 1; EINVAL on a sharded ctx. */
