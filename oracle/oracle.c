@@ -38,9 +38,24 @@
 #include <stdint.h>
 #include <string.h>
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 #if FLT_EVAL_METHOD != 0
 #error "orc_accumulate32 needs binary32 evaluation of float expressions (FLT_EVAL_METHOD 0)"
 #endif
+
+/* OpenMP thread count of the element loops (results do not depend on it); returns the count now in effect */
+int orc_set_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+    return omp_get_max_threads();
+#else
+    (void)t;
+    return 1;
+#endif
+}
 
 /* ------------------------------------------------------------------ binary16 codec
  * IEEE 754 binary16: 1 sign bit, 5 exponent bits (bias 15), 10 mantissa bits.

@@ -58,6 +58,8 @@ def lib():
         L.orc_h_nonfinite.argtypes = [u16]
         L.orc_h2d_array.argtypes = [p, p, i64]
         L.orc_d2h_array.argtypes = [p, p, i64]
+        L.orc_set_threads.restype = i32
+        L.orc_set_threads.argtypes = [i32]
         L.orc_accumulate.argtypes = [p, p, i64, i32]
         L.orc_accumulate32.argtypes = [p, p, i64, i32]
         L.orc_round16.argtypes = [p, p, i64]
@@ -107,6 +109,11 @@ def d2h_array(x: np.ndarray) -> np.ndarray:
     out = np.empty(x.size, dtype=np.uint16)
     lib().orc_d2h_array(_p(x), _p(out), x.size)
     return out
+
+
+def set_threads(t: int) -> int:
+    """OpenMP threads of the oracle's element loops (t <= 0: query); returns the count in effect."""
+    return lib().orc_set_threads(t)
 
 
 def lr_at(t: int, peak: float = 5e-4, warmup: int = 4000) -> float:
