@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline leg")
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="--impl reference: oracle seconds for the whole run, spread over the steps")
     return ap.parse_args()
 
 
@@ -180,7 +182,7 @@ def run_reference(args):
     if rank != 0:
         return
     wl = workload(args.config, args.gpus, args.update_freq)
-    per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    per_step = max(0.1, args.ref_seconds / max(1, args.steps + args.warmup))
     vals = []
     for _ in range(args.warmup):
         oracle_rate(wl, per_step * 0.25)
