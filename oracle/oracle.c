@@ -31,7 +31,8 @@
  * scaler S:91-94 examples + torch._amp_update_scale_ + closed-form traces;
  * LR S:196-199 + fp32 bit patterns; Adam S:206-208 + constant-gradient closed
  * form + torch.optim.Adam in fp64; reduce S:390-393; large-batch equivalence
- * on a brute-force softmax-regression model.
+ * on a brute-force softmax-regression model; the fp32-accumulator variant
+ * (SURVEY Z1 knob) against numpy's binary32 adds + hand-worked special cases.
  */
 #include <float.h>
 #include <math.h>
