@@ -3,9 +3,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config big_ende|base|tiny] [--impl ours|reference]
 
-One step = one whole update: update_freq x accumulate (K1) + bucketed NCCL all-reduce (W > 1, K1s) + step
-(K0 + K2), on synthetic Transformer-shaped fp16 micro-gradients already resident in HBM.  N > 1 is launched
-by torchrun (one process per GPU); rank 0 prints ONE JSON line.  Metric and config: BASELINE.json
+One step = one whole update: update_freq x accumulate (K1) + bucketed all-reduce (W > 1) + step (decision + Adam),
+on synthetic Transformer-shaped fp16 micro-gradients already resident in HBM.  N > 1: one process per GPU, launched
+by torchrun or, without it, by bench.py itself; rank 0 prints ONE JSON line.  At W > 1 the headline is the paper's
+replicated update, with the sharded variant (f2) beside it.  Metric and config: BASELINE.json
 (configs[2], Transformer-big En-De, update_freq 16, at 1/2/4/8 B200).
 """
 from __future__ import annotations
@@ -40,10 +41,10 @@ def parse():
     ap.add_argument("--bucket-mib", type=float, default=150.0)
     ap.add_argument("--allreduce", choices=["auto", "nccl", "fused"], default="auto")
     ap.add_argument("--optimizer", choices=["auto", "sharded", "replicated"], default="auto",
-                    help="W > 1 update layout. sharded = SURVEY f2: reduce-scatter + Adam on 1/W + all-gather of "
-                         "w16 (bitwise equal to the paper's replicated update, tests/test_gpu_multi.py); "
-                         "replicated = every rank updates the whole vector (the paper's layout); auto = sharded "
-                         "when the fused all-reduce is available, else replicated")
+                    help="W > 1 update layout of the headline. replicated = every rank updates the whole vector (the "
+                         "paper's layout, SURVEY 8(e)); sharded = SURVEY f2: reduce-scatter + Adam on 1/W + "
+                         "all-gather of w16 (bitwise equal to the replicated update); auto = replicated headline "
+                         "with the sharded variant timed beside it when the fused all-reduce is available")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
     ap.add_argument("--generator", choices=["real", "exact", "zero"], default="real",
                     help="input family (SURVEY 8(d.2)); the performance-independence check times all three")
@@ -159,7 +160,7 @@ def oracle_rate(wl, seconds, slice_elems=2_000_000):
     toks = [[synth.ntokens(wl, 1, r, k) for k in range(1, c + 1)] for r in range(W)]
     t0 = time.perf_counter()
     n_up = 0
-    while True:
+    while True:                        # seconds = 0: exactly one whole update of the slice
         orc.update(grads, toks)
         n_up += 1
         if time.perf_counter() - t0 >= seconds:
@@ -177,30 +178,97 @@ def omp_threads():
     return O.set_threads(0)
 
 
+def cpu_model():
+    """Host CPU model (lscpu 'Model name'), for the oracle baselines."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def plan_buckets_host(numel, bucket_bytes):
+    """The paper's bucket rule (reading R17) restated for the reference arm's config description only: greedy
+    in ready order, whole tensors, close at >= threshold, remainder last.  (The product's plan is smpu_plan_buckets.)"""
+    n_b, cur = 0, 0
+    for x in numel:
+        cur += 2 * int(x)
+        if cur >= bucket_bytes:
+            n_b, cur = n_b + 1, 0
+    return n_b + (1 if cur else 0)
+
+
+def bench_config(args, wl, world, toks_per_update, path_bytes_per_elem, sharded=False, fused=None, n_buckets=None):
+    """`config` of the JSON line -- identical keys (and values) for both arms, so the driver can match them."""
+    c = wl.update_freq
+    if fused is None:
+        fused = world == 1 and args.fuse_final == 1 and not args.accum_fp32
+    if n_buckets is None:
+        n_buckets = plan_buckets_host(wl.numel, int(args.bucket_mib * (1 << 20)))
+    return {"workload": wl.name, "n_params": wl.n, "n_tensors": len(wl.numel), "update_freq": c, "world": world,
+            "bucket_mib": args.bucket_mib, "n_buckets": n_buckets, "tokens_per_update": int(toks_per_update),
+            "generator": {"real": "G_real", "exact": "G_exact", "zero": "zeros"}[args.generator] + " (SURVEY 8(d.2))",
+            "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
+            "path_bytes_per_elem": path_bytes_per_elem,
+            "optimizer": "sharded (SURVEY f2)" if (sharded and world > 1) else "replicated (paper)",
+            "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"}
+
+
+def path_bpe(c, world, fused, acc32):
+    """Algorithmic HBM bytes per parameter of one update."""
+    if fused:
+        return (4 if c > 1 else 0) + 6 * max(c - 2, 0) + (30 if c > 1 else 28)
+    if acc32:
+        return 6 + 10 * (c - 2) + 8 + 28 if c > 1 else 32
+    return 4 + 6 * (c - 1) + 28
+
+
 def run_reference(args):
+    """This tier's reference arm: the CPU oracle as it stands, on the box's host cores.  Each step is one whole
+    oracle update (all c micro-batches of all W ranks, emulated) over a bounded contiguous slice of the workload's
+    parameter vector, sized so the whole --steps/--warmup run takes about --ref-seconds; `ms_per_step` is the
+    measured wall time of such a step, so ms_per_step x steps is what actually ran.  `value` = grad elements per
+    second of those steps (the metric's unit); the full-vector update time is extrapolated beside it, labelled."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     wl = workload(args.config, args.gpus, args.update_freq)
-    per_step = max(0.1, args.ref_seconds / max(1, args.steps + args.warmup))
-    vals = []
+    wl.family = args.generator
+    W, c = wl.world, wl.update_freq
+    # probe: one update on a small slice gives the oracle's rate; then size the slice for the budget
+    probe_v, probe_s, _ = oracle_rate(wl, 0.0, slice_elems=min(wl.n, 1 << 18))
+    per_step = max(0.05, args.ref_seconds / max(1, args.steps + args.warmup))
+    slice_elems = int(min(wl.n, max(1 << 16, probe_v * per_step / (W * c))))
     for _ in range(args.warmup):
-        oracle_rate(wl, per_step * 0.25)
-    secs = []
+        oracle_rate(wl, 0.0, slice_elems=slice_elems)
+    vals, secs = [], []
     for _ in range(args.steps):
-        v, s, sample = oracle_rate(wl, per_step)
+        v, sec, sample = oracle_rate(wl, 0.0, slice_elems=slice_elems)
         vals.append(v)
-        secs.append(s)
+        secs.append(sec)
     value = statistics.median(vals)
+    fused = W == 1 and args.fuse_final == 1 and not args.accum_fp32
+    toks = sum(synth_ntokens(wl, 1, r, k) for r in range(W) for k in range(1, c + 1))
+    cfg = bench_config(args, wl, W, toks, path_bpe(c, W, fused, args.accum_fp32 and c > 1))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wl.world * wl.update_freq * wl.n / value,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+binary16",
-            "data": "synthetic", "config": {"workload": wl.name, "n_params": wl.n, "update_freq": wl.update_freq,
-                                             "world": wl.world},
+            "data": "synthetic", "config": cfg,
+            "step_is": f"one whole oracle update over elements [0, {slice_elems}) of {wl.n} (all {W}x{c} "
+                       f"micro-batches), not the full vector",
+            "full_update_ms_extrapolated": 1000 * W * c * wl.n / value,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def synth_ntokens(wl, u, r, k):
+    import synth
+    return synth.ntokens(wl, u, r, k)
 
 
 # ------------------------------------------------------------------------------------------ M2 backward load
@@ -369,6 +437,127 @@ def run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg,
 
 
 # ------------------------------------------------------------------------------------------ our arm
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def own_launches(stats, ar_impl, nccl_impl):
+    """Kernels of libsmpu.so in `stats` (every kind, except the all-reduces when NCCL runs them)."""
+    lib_kinds = ("allreduce", "decision_ar") if ar_impl == nccl_impl else ()
+    return int(sum(v["launches"] for k, v in stats.items() if k not in lib_kinds))
+
+
+def measure(args, step, grads, toks, stream, world, local, resident=True):
+    """Time one ctx: a call-by-call region (kernel events -> per-kernel table, roofline) and the captured CUDA graph of
+    the same update (the headline unless --no-graph), each after warm-up and a ~0.6 s soak under the clock sampler,
+    bracketed by barrier + synchronize, CUDA events on the launch stream, max over ranks."""
+    import torch
+    c = len(grads)
+
+    def one_update():
+        for k in range(c):
+            step.accumulate(grads[k], toks[k], stream)
+        step.step(stream, wait=False)
+
+    t_w = time.perf_counter()
+    for _ in range(args.warmup):
+        one_update()
+    torch.cuda.synchronize()
+    per_update = _max_over_ranks((time.perf_counter() - t_w) / max(1, args.warmup), world)
+    soak = max(2, min(2000, int(0.6 / max(per_update, 1e-5))))     # same count on every rank (collectives)
+    _barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        for _ in range(soak):
+            one_update()
+        step.kernel_stats(reset=True)
+        step.set_timing(True)
+        torch.cuda.synchronize()
+        _barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_update()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        _barrier(world)
+    step.set_timing(False)
+    out = {"ms_calls": ev0.elapsed_time(ev1) / args.steps, "clk": clk}
+    out["ms"] = out["ms_calls"]
+    if args.trace:
+        with open(args.trace if world == 1 else f"{args.trace}.rank{step.rank}", "w") as f:
+            for kname, sname, a, b in step.kernel_trace():
+                f.write(json.dumps({"rank": step.rank, "kernel": kname, "stream": sname, "start_ms": round(a, 4),
+                                    "end_ms": round(b, 4)}) + "\n")
+    out["stats"] = step.kernel_stats(reset=True)
+    last = step.result(step.scalars()["attempts"])
+    assert last["applied"] == 1 and last["overflow"] == 0, last
+    out["graph"] = None
+    if args.no_graph:
+        return out
+    import paper_1806_00187_b200 as P
+    try:
+        step.graph_capture(grads)
+    except P.SmpuError as ex:          # e.g. W > 1 fell back to NCCL (not graph-capturable here)
+        print(f"[bench] graph capture unavailable ({ex}); timing the call-by-call path", file=sys.stderr)
+        return out
+    for _ in range(args.warmup):
+        step.graph_launch(toks, stream)
+    torch.cuda.synchronize()
+    _barrier(world)
+    with Clocks(local) as clk_g:
+        for _ in range(soak):
+            step.graph_launch(toks, stream)
+        step.kernel_stats(reset=True)
+        torch.cuda.synchronize()
+        _barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step.graph_launch(toks, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        _barrier(world)
+    out["ms"] = ev0.elapsed_time(ev1) / args.steps
+    out["gstats"] = step.kernel_stats(reset=True)
+    out["clk"] = clk_g
+    last = step.result(step.scalars()["attempts"])
+    assert last["applied"] == 1 and last["overflow"] == 0, last
+    out["graph"] = {"ms_per_step_graph": out["ms"], "ms_per_step_calls": out["ms_calls"]}
+    if resident:
+        # variant: the producer keeps all c micro-batch gradients resident (6.7 GB of 180 GB) and the update
+        # accumulates them in one pass (smpu_accumulate_many; bitwise the same sums) -- reported beside the
+        # headline, which keeps the paper's in-place accumulation after every micro-batch
+        step.graph_capture(grads, resident=True)
+        for _ in range(args.warmup):
+            step.graph_launch(toks, stream)
+        torch.cuda.synchronize()
+        _barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step.graph_launch(toks, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        _barrier(world)
+        out["ms_resident"] = _max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+        last = step.result(step.scalars()["attempts"])
+        assert last["applied"] == 1 and last["overflow"] == 0, last
+    return out
+
+
+def bus_gbs(stats, steps, n, world, sharded):
+    """In-situ bus bandwidth of the bucket all-reduce (nccl-tests convention): all-reduce 2(W-1)/W x 2n bytes per
+    update; the sharded layout's timed kernel is the reduce-scatter alone, (W-1)/W x 2n (its w16 all-gather is peer
+    stores inside the Adam kernel)."""
+    ar_ms = stats["allreduce"]["ms"] / steps
+    if ar_ms <= 0:
+        return None
+    phases = 1 if sharded else 2
+    bus = phases * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9
+    return {"ms_per_step": ar_ms, "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS,
+            "frac_of_770_measured_peer": bus / 770.0, "in_situ": "concurrent with K1 / Adam"}
+
+
 def main_ours(args):
     import torch
     import torch.distributed as dist
@@ -384,17 +573,18 @@ def main_ours(args):
 
     import paper_1806_00187_b200 as P
     import synth
-    from paper_1806_00187_b200 import smpu
 
     wl = workload(args.config, world, args.update_freq)
     wl.family = args.generator
     lay = synth.Layout(wl)
     c, n = wl.update_freq, lay.n
-    nccl_id = None
-    if world > 1:
+
+    def new_id():
+        if world == 1:
+            return None
         obj = [P.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
 
     # inputs resident in HBM: theta_0 and c micro-gradient buffers of this rank (update u = 1, e = 7)
     theta0 = torch.empty(n, dtype=torch.float32, device="cuda")
@@ -405,34 +595,23 @@ def main_ours(args):
         synth.micro_grad_gpu(g, wl, lay, 1, rank, k, 7)
         grads.append(g)
     toks = [synth.ntokens(wl, 1, rank, k) for k in range(1, c + 1)]
-    want_shard = world > 1 and args.allreduce != "nccl" and (args.optimizer == "sharded" or args.sharded or
-                                                             args.optimizer == "auto")
-    cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)),
-                           allreduce={"auto": 0, "nccl": 1, "fused": 2}[args.allreduce], sharded=int(want_shard),
-                           fuse_final=args.fuse_final, accum_fp32=int(args.accum_fp32))
+    toks_all = _sum_over_ranks(sum(toks), world)
+    # the headline layout: the paper's replicated update; --optimizer sharded makes f2 the headline
+    head_sharded = world > 1 and (args.optimizer == "sharded" or args.sharded)
+    ar = {"auto": 0, "nccl": 1, "fused": 2}[args.allreduce]
+
+    def make_cfg(sharded, fuse_final=args.fuse_final):
+        cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)), allreduce=ar,
+                               sharded=int(sharded), fuse_final=fuse_final, accum_fp32=int(args.accum_fp32))
+        # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
+        cfg.growth_interval = 1 << 40
+        return cfg
+
     fused = world == 1 and args.fuse_final == 1 and not args.accum_fp32
     acc32 = args.accum_fp32 and c > 1
-    # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
-    cfg.growth_interval = 1 << 40
     torch.cuda.synchronize()
-    try:
-        step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
-    except P.SmpuError as ex:
-        # auto: the sharded layout needs the fused all-reduce (an LSA window over NVLink); without it every
-        # rank refuses the same way, and all fall back to the paper's replicated update together
-        if not (want_shard and args.optimizer == "auto" and not args.sharded and ex.status == P.smpu.EINVAL):
-            raise
-        print(f"[bench] sharded optimizer unavailable ({ex}); replicated update", file=sys.stderr, flush=True)
-        want_shard = False
-        cfg.sharded = 0
-        if rank == 0:
-            nccl_id = P.unique_id()
-        if world > 1:
-            obj = [nccl_id]
-            dist.broadcast_object_list(obj, src=0)
-            nccl_id = obj[0]
-        step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=nccl_id, device=local)
-    args.sharded = want_shard
+    cfg = make_cfg(head_sharded)
+    step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=new_id(), device=local)
     ar_impl = step.allreduce_impl
     stream = torch.cuda.current_stream()
     if args.mode == "m2":
@@ -444,141 +623,10 @@ def main_ours(args):
             dist.destroy_process_group()
         return
 
-    def own_launches(st):
-        # every kind is a kernel of libsmpu.so, except the all-reduces when NCCL runs them
-        lib_kinds = ("allreduce", "decision_ar") if ar_impl == P.smpu.AR_NCCL else ()
-        return int(sum(v["launches"] for k, v in st.items() if k not in lib_kinds))
-
-    def one_update():
-        for k in range(c):
-            step.accumulate(grads[k], toks[k], stream)
-        step.step(stream, wait=False)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    t_w = time.perf_counter()
-    for _ in range(args.warmup):
-        one_update()
-    torch.cuda.synchronize()
-    per_update = _max_over_ranks((time.perf_counter() - t_w) / max(1, args.warmup), world)
-    soak = max(2, min(2000, int(0.6 / max(per_update, 1e-5))))     # same count on every rank (NCCL)
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        # soak under the same load for ~0.6 s so that the 100 ms clock sampler sees the timed region's state
-        for _ in range(soak):
-            one_update()
-        step.kernel_stats(reset=True)
-        step.set_timing(True)
-        torch.cuda.synchronize()
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            one_update()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-    step.set_timing(False)
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms_calls = ms
-    if args.trace:
-        with open(args.trace if world == 1 else f"{args.trace}.rank{rank}", "w") as f:
-            for kname, sname, a, b in step.kernel_trace():
-                f.write(json.dumps({"rank": rank, "kernel": kname, "stream": sname, "start_ms": round(a, 4),
-                                    "end_ms": round(b, 4)}) + "\n")
-    stats = step.kernel_stats(reset=True)
-    last = step.result(step.scalars()["attempts"])
-    assert last["applied"] == 1 and last["overflow"] == 0, last
-
-    # ---- the same update as one CUDA graph (the headline unless --no-graph): per-kernel event timing cannot see
-    # inside a graph, so the kernel table / roofline above come from the call-by-call region, same kernels
-    graph_info = None
-    if not args.no_graph:
-        try:
-            step.graph_capture(grads)
-        except P.SmpuError as ex:          # e.g. W > 1 fell back to NCCL (not graph-capturable here)
-            print(f"[bench] graph capture unavailable ({ex}); timing the call-by-call path", file=sys.stderr)
-            args.no_graph = True
-    if not args.no_graph:
-        for _ in range(args.warmup):
-            step.graph_launch(toks, stream)
-        torch.cuda.synchronize()
-        barrier()
-        with Clocks(local) as clk_g:
-            for _ in range(soak):
-                step.graph_launch(toks, stream)
-            step.kernel_stats(reset=True)
-            torch.cuda.synchronize()
-            barrier()
-            ev0.record(stream)
-            for _ in range(args.steps):
-                step.graph_launch(toks, stream)
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            barrier()
-        ms = ev0.elapsed_time(ev1) / args.steps
-        gstats = step.kernel_stats(reset=True)
-        last = step.result(step.scalars()["attempts"])
-        assert last["applied"] == 1 and last["overflow"] == 0, last
-        clk = clk_g
-        graph_info = {"ms_per_step_graph": ms, "ms_per_step_calls": ms_calls,
-                      "launches_per_step": own_launches(gstats) / args.steps}
-        # variant: the producer keeps all c micro-batch gradients resident (6.7 GB of 180 GB) and the update
-        # accumulates them in one pass (smpu_accumulate_many; bitwise the same sums) -- reported beside the
-        # headline, which keeps the paper's in-place accumulation after every micro-batch
-        step.graph_capture(grads, resident=True)
-        for _ in range(args.warmup):
-            step.graph_launch(toks, stream)
-        torch.cuda.synchronize()
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step.graph_launch(toks, stream)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        ms_res = _max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
-        last = step.result(step.scalars()["attempts"])
-        assert last["applied"] == 1 and last["overflow"] == 0, last
-        # one pass over the c gradients (+ the accumulator written, then Adam's 28) or, fused, straight into Adam
-        res_bpe = (10 * c + 22) if acc32 else (2 * c + 26 if fused else 2 * c + 2 + 28)   # fp32 acc.: streaming
-        res_bytes = n * res_bpe
-        graph_info["resident_microbatches"] = {
-            "ms_per_step": ms_res, "value": world * c * n / (ms_res * 1e-3), "unit": UNIT,
-            "path_hbm_gbs": res_bytes / (ms_res * 1e-3) / 1e9, "bytes_per_elem": res_bpe,
-            "api": "smpu_graph_capture(..., SMPU_GRAPH_RESIDENT) -> one smpu_accumulate_many over c buffers"}
-
-    # ---- exposed communication: the same per-GPU work through a world = 1 ctx on the same GPU
-    exposed = None
-    if world > 1:
-        cfg.fuse_final = 0     # the world > 1 kernels (accumulate, decide, Adam), minus the exchange
-        step1 = P.UpdateStep(wl.numel, theta0, cfg, world=1, rank=0, device=local)
-
-        if not args.no_graph:
-            step1.graph_capture(grads)
-
-        def one_update1():
-            if not args.no_graph:
-                step1.graph_launch(toks, stream)
-                return
-            for k in range(c):
-                step1.accumulate(grads[k], toks[k], stream)
-            step1.step(stream, wait=False)
-        for _ in range(args.warmup):
-            one_update1()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            one_update1()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t1 = _max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-        step1.close()
-        del step1
-        exposed = t1
+    M = measure(args, step, grads, toks, stream, world, local)
+    ms, ms_calls, stats = M["ms"], M["ms_calls"], M["stats"]
+    nb = step.n_buckets
+    shard = sum(h - l for l, h in step.shard_ranges())
 
     # ---- end-to-end through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
@@ -586,29 +634,54 @@ def main_ours(args):
         pool = min(c, 4)
         host = [grads[k].cpu().pin_memory() for k in range(pool)]
         torch.cuda.synchronize()
-        barrier()
-        for _ in range(1):
-            for k in range(c):
-                step.accumulate(host[k % pool], toks[k], stream)
-            step.step(stream, wait=True)
-        barrier()
+        _barrier(world)
+        for k in range(c):
+            step.accumulate(host[k % pool], toks[k], stream)
+        step.step(stream, wait=True)
+        _barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             for k in range(c):
                 step.accumulate(host[k % pool], toks[k], stream)
-            res = step.step(stream, wait=True)          # device -> host read of the step's result
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        e2e_s = _max_over_ranks(e2e_s, world)
+            step.step(stream, wait=True)          # device -> host read of the step's result
+        e2e_s = _max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, world)
         e2e = {"value": world * c * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": c * n * 2,
                "d2h_bytes_per_step": ctypes_sizeof_result(), "ms_per_step": 1000 * e2e_s,
                "source": "pinned host fp16 micro-gradients, staged H2D inside smpu_accumulate"}
         del host
+    step.close()
+    del step
+
+    # ---- W > 1: the sharded layout beside the replicated headline, same inputs
+    variant = None
+    if world > 1 and not head_sharded and args.optimizer == "auto" and ar_impl == P.smpu.AR_FUSED:
+        sstep = P.UpdateStep(wl.numel, theta0, make_cfg(True), world=world, rank=rank, nccl_id=new_id(), device=local)
+        V = measure(args, sstep, grads, toks, stream, world, local, resident=False)
+        variant = {"ms_per_step": _max_over_ranks(V["ms"], world), "ms_per_step_calls": _max_over_ranks(V["ms_calls"], world),
+                   "allreduce": bus_gbs({k: {"ms": _max_over_ranks(v["ms"], world)} for k, v in V["stats"].items()},
+                                        args.steps, n, world, True),
+                   "shard_elems": sum(h - l for l, h in sstep.shard_ranges())}
+        variant["value"] = world * c * n / (variant["ms_per_step"] * 1e-3)
+        variant["update_steps_per_s"] = 1000.0 / variant["ms_per_step"]
+        sstep.close()
+        del sstep
+
+    # ---- exposed communication: the same per-GPU work through a world = 1 ctx on the same GPU (fuse_final = 0:
+    # the W > 1 kernels -- accumulate, decide, Adam over all n -- minus the exchange)
+    t1 = k2_full_ms = None
+    if world > 1:
+        step1 = P.UpdateStep(wl.numel, theta0, make_cfg(False, fuse_final=0), world=1, rank=0, device=local)
+        B = measure(args, step1, grads, toks, stream, 1, local, resident=False)
+        t1 = _max_over_ranks(B["ms"], world)
+        k2_full_ms = _max_over_ranks(B["stats"]["k2_adam"]["ms"] / args.steps, world)
+        step1.close()
+        del step1
 
     ms = _max_over_ranks(ms, world)
     ms_calls = _max_over_ranks(ms_calls, world)
     kstat = {k: {"launches": v["launches"], "ms": _max_over_ranks(v["ms"], world)} for k, v in stats.items()}
+    ms_res = M.get("ms_resident")
     if rank != 0:
-        step.close()
         if world > 1:
             dist.destroy_process_group()
         return
@@ -616,12 +689,10 @@ def main_ours(args):
     peaks = measured_peaks()
     hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
     peak_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "of fallback (B200_PROFILING.md)"
-    nb = step.n_buckets
     # algorithmic bytes per launch: K1 first 4 B/elem, K1 add 6, K1s 2, K2 28, K12 (the
     # fused last micro-batch + Adam, W = 1) 30 (28 at c = 1: no accumulator read)
     # (K1s only sweeps when the early decision was undecided; with G_real it returns at once)
     # with the fp32 accumulator (Z1 knob): first 6 B/elem, add 10, the last micro-batch 8 (rn16 into acc16)
-    shard = sum(h - l for l, h in step.shard_ranges())
     if fused:
         step_bytes = {"k1_first": 4 * n if c > 1 else 0, "k1_add": 6 * max(c - 2, 0) * n, "k2_adam": 0,
                       "k12_fused": (30 if c > 1 else 28) * n}
@@ -650,37 +721,53 @@ def main_ours(args):
     out = {"metric": METRIC, "value": world * c * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f16+f32", "data": "synthetic",
-           "config": {"workload": wl.name, "n_params": n, "n_tensors": len(wl.numel), "update_freq": c,
-                      "world": world, "bucket_mib": args.bucket_mib, "n_buckets": nb,
-                      "tokens_per_update": int(sum(toks)) * world, "generator": {"real": "G_real", "exact": "G_exact", "zero": "zeros"}[args.generator] + " (SURVEY 8(d.2))",
-                      "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
-                      "path_bytes_per_elem": path_bytes / n,
-                      "optimizer": "sharded (SURVEY f2)" if (args.sharded and world > 1) else "replicated (paper)", "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"},
+           "config": bench_config(args, wl, world, toks_all, path_bytes / n, sharded=head_sharded, fused=fused,
+                                  n_buckets=nb),
            "update_steps_per_s": 1000.0 / ms,
            "path_hbm_gbs": path_bytes / (ms * 1e-3) / 1e9,
            "path_hbm_frac": path_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
            "roofline": roof, "kernels": kernels,
            # our kernels in the timed region (the graph replays' when the graph is timed)
-           "gpu_launches": own_launches(stats if args.no_graph else gstats),
-           "clocks": clk.summary(),
-           "timed_path": "calls (c x smpu_accumulate + smpu_step)" if args.no_graph else
+           "gpu_launches": own_launches(M["gstats"] if M["graph"] else stats, ar_impl, P.smpu.AR_NCCL),
+           "clocks": M["clk"].summary(),
+           "timed_path": "calls (c x smpu_accumulate + smpu_step)" if not M["graph"] else
                          "cuda_graph (smpu_graph_launch of the captured update; kernels/roofline from the call path)"}
-    if graph_info:
-        out["graph"] = {k: (_max_over_ranks(v, 1) if isinstance(v, float) else v) for k, v in graph_info.items()}
-    if exposed is not None:
-        out["exposed_comm"] = {"ms": ms - exposed, "frac_of_update": (ms - exposed) / ms, "t_world1_ms": exposed,
+    if M["graph"]:
+        g = dict(M["graph"])
+        g["launches_per_step"] = own_launches(M["gstats"], ar_impl, P.smpu.AR_NCCL) / args.steps
+        if ms_res:
+            # one pass over the c gradients (+ the accumulator written, then Adam's 28) or, fused, straight into Adam
+            res_bpe = (10 * c + 22) if acc32 else (2 * c + 26 if fused else 2 * c + 2 + 28)
+            g["resident_microbatches"] = {
+                "ms_per_step": ms_res, "value": world * c * n / (ms_res * 1e-3), "unit": UNIT,
+                "path_hbm_gbs": n * res_bpe / (ms_res * 1e-3) / 1e9, "bytes_per_elem": res_bpe,
+                "api": "smpu_graph_capture(..., SMPU_GRAPH_RESIDENT) -> one smpu_accumulate_many over c buffers"}
+        out["graph"] = g
+    if t1 is not None:
+        out["exposed_comm"] = {"ms": ms - t1, "frac_of_update": (ms - t1) / ms, "t_world1_ms": t1,
+                               "layout": "sharded (SURVEY f2)" if head_sharded else "replicated (paper)",
                                "method": "T(update, W ranks) - T(same per-GPU work through a world=1 ctx, same "
-                                         "GPU, same run); library-only step (no backward to hide behind)"}
-    if world > 1 and kstat["allreduce"]["ms"] > 0:
-        ar_ms = kstat["allreduce"]["ms"] / args.steps
-        # bus bytes per rank (nccl-tests convention): all-reduce 2(W-1)/W x 2n; the sharded layout's timed kernel is
-        # the reduce-scatter alone, (W-1)/W x 2n (its all-gather of w16 is peer stores inside the Adam kernel)
-        phases = 1 if args.sharded else 2
-        bus = phases * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9
-        out["allreduce"] = {"impl": {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)) +
-                            ("_reduce_scatter" if args.sharded else ""), "ms_per_step": ar_ms,
-                            "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS,
-                            "frac_of_770_measured_peer": bus / 770.0, "in_situ": "concurrent with K1 / Adam"}
+                                         "GPU, same run, fuse_final=0); library-only step (no backward to hide "
+                                         "behind)"}
+        if head_sharded:
+            base = t1 - k2_full_ms * (1 - 1 / world)
+            out["exposed_comm"].update(ms=ms - base, frac_of_update=(ms - base) / ms, t_world1_ms=base,
+                                       method="estimate: world=1 time with its Adam share (CUDA events) scaled to "
+                                              "the shard, 1/W of it")
+    if world > 1:
+        a = bus_gbs(kstat, args.steps, n, world, head_sharded)
+        if a:
+            a["impl"] = {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)) + ("_reduce_scatter" if head_sharded else "")
+            out["allreduce"] = a
+    if variant:
+        base = t1 - k2_full_ms * (1 - 1 / world)
+        variant["exposed_comm_estimate"] = {
+            "ms": variant["ms_per_step"] - base, "frac_of_update": (variant["ms_per_step"] - base) / variant["ms_per_step"],
+            "t_baseline_ms": base,
+            "method": "T(sharded update, W ranks) - [T(world=1 ctx) - (1 - 1/W) x its Adam time]: the same per-GPU "
+                      "work (K1 passes over n, Adam over n/W) without the exchange, estimated"}
+        variant["layout"] = "sharded (SURVEY f2): reduce-scatter, Adam on 1/W, w16 all-gathered by peer stores; bitwise the replicated update (tests/test_gpu_virtual.py, test_gpu_multi.py)"
+        out["sharded_variant"] = variant
     if e2e:
         out["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:
@@ -692,9 +779,8 @@ def main_ours(args):
         v1, _, sample1 = oracle_rate(wl, max(2.0, args.cpu_seconds / 4))
         O.set_threads(cores)
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-                               "value_1_thread": v1, "sample_1_thread": sample1}
+                               "value_1_thread": v1, "sample_1_thread": sample1, "cpu_model": cpu_model()}
     print(json.dumps(out), flush=True)
-    step.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -716,6 +802,34 @@ def _max_over_ranks(x, world):
     return float(t.item())
 
 
+def _sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([int(x)], dtype=torch.int64, device=dev)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without torchrun: launch N ranks of this same command, one process per GPU, on 127.0.0.1 (the
+    environment torchrun would give them); rank 0 prints the line.  Exit status: the worst rank's."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rcs = [p.wait() for p in procs]
+    bad = [rc for rc in rcs if rc != 0]
+    sys.exit(bad[0] if bad else 0)
+
+
 def load_traffic(kernel, workload_name):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -729,6 +843,9 @@ def load_traffic(kernel, workload_name):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -39,10 +39,11 @@
 extern "C" {
 #endif
 
-#define SMPU_ABI_VERSION 2
+#define SMPU_ABI_VERSION 3
 #define SMPU_NCCL_ID_BYTES 128
 
 typedef struct smpu_ctx smpu_ctx;
+typedef struct smpu_group smpu_group;   /* W virtual ranks on one GPU (smpu_group_init) */
 
 typedef enum {
     SMPU_OK = 0,
@@ -87,6 +88,18 @@ typedef struct {
                                   buckets of bucket_bytes (rounded up to 128 elements) cut wherever they fall, so a
                                   tensor may span buckets (smpu_tensor_ready then counts it in each).  Buckets
                                   change timing, never values.                                        */
+    /* Shape of the fused all-reduce (world > 1, SMPU_AR_FUSED).  They decide the number of NCCL LSA barriers and
+       whether the device communicator needs NVLS multicast -- collective resources -- so every rank must pass the
+       same values: smpu_init compares them (and the fields above) across ranks and returns SMPU_EINVAL on EVERY rank
+       when they differ, instead of hanging.  They never change results (the sum order is fixed), only speed.      */
+    int32_t ar_ctas;           /* CTAs per rank of each bucket all-reduce; 0 (default) = one per SM                 */
+    int32_t ar_threads;        /* threads per CTA: 256 (default) or 512                                             */
+    int32_t ar_vec_bytes;      /* bytes per peer load / store: 32 (default, 256-bit) or 16                           */
+    int32_t ar_unroll;         /* 32-byte units in flight per thread: 1 (default) or 2                               */
+    int32_t ar_mcast;          /* 1: all-gather by NVLS multicast stores (multimem.st; EINVAL on every rank if some
+                                  rank has no NVLS); 0 (default): unicast peer stores                                 */
+    int32_t pdl;               /* world == 1: programmatic dependent launch of the K1 -> K0 -> K2 chain, 1 (default)
+                                  or 0.  Per rank; no effect at world > 1.                                           */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */
@@ -165,6 +178,26 @@ smpu_status smpu_plan_shards(const int64_t* bucket_begin, int n_buckets, int wor
  * second theta/m/v of fuse_final at world 1). */
 smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
                       int cuda_device, const int64_t* numel, int n_tensors, const float* init_params);
+
+/* A VIRTUAL world: `world` (2..8) data-parallel ranks held on ONE GPU, for running and checking the world > 1 path
+ * (bucketed all-reduce, exact early / late overflow decision, sharded optimizer)
+ * without W GPUs.  Each member is a full ctx -- its own theta/m/v/w16/accumulator and scaler state, packed as for
+ * smpu_init -- whose "window" is a plain device allocation; the peer kernels are the very kernels of the NCCL path
+ * (lsa_allreduce.cuh), instantiated over local windows instead of NVLink peers: one launch covers every rank and
+ * kernel boundaries replace the LSA barriers.  Sums are in ascending rank order, as with SMPU_AR_FUSED.
+ *   cfg          host; copied.  allreduce must not be SMPU_AR_NCCL and ar_mcast must be 0 (EINVAL).
+ *   numel, init_params   as smpu_init; every member starts from the same theta_0.
+ * Members (smpu_group_member) take the smpu_* calls of a rank, driven from one host thread in any interleaving a
+ * W-process job could produce, with two rules: every member gives its c micro-batches before any member calls
+ * smpu_step (ESTATE otherwise), and a member that stepped starts its next update only after every member stepped
+ * (ESTATE).  A collective step runs when the last member reaches it.  Sharded (cfg->sharded): the update of every
+ * member completes when the last one steps, so smpu_step(out != NULL) is ESTATE before that -- pass NULL and read
+ * smpu_result.  Not available on members: smpu_graph_capture, smpu_allreduce_accumulator (EINVAL).
+ * smpu_destroy on a member is a no-op; smpu_group_destroy frees the group and its members. */
+smpu_status smpu_group_init(smpu_group** out, const smpu_config* cfg, int world, int cuda_device, const int64_t* numel,
+                            int n_tensors, const float* init_params);
+smpu_status smpu_group_member(smpu_group* group, int rank, smpu_ctx** member);
+void smpu_group_destroy(smpu_group* group);
 
 smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n);
 

@@ -5,10 +5,10 @@ this package is its thin binding.  Importing it loads the library and fails
 loudly if it has not been built: there is no CPU fallback.
 """
 from . import smpu
-from .smpu import (Config, SmpuError, StepResult, UpdateStep, abi_version, config_default,  # noqa: F401
-                   plan_buckets, unique_id)
+from .smpu import (Config, SmpuError, StepResult, UpdateStep, VirtualGroup, abi_version,  # noqa: F401
+                   config_default, plan_buckets, unique_id)
 
 smpu.lib()  # load now: a missing extension is an import error, never a silent fallback
 
-__all__ = ["smpu", "Config", "SmpuError", "StepResult", "UpdateStep", "abi_version", "config_default",
+__all__ = ["smpu", "Config", "SmpuError", "StepResult", "UpdateStep", "VirtualGroup", "abi_version", "config_default",
            "plan_buckets", "unique_id"]

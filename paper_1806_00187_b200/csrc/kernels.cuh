@@ -86,9 +86,8 @@ __device__ __forceinline__ void st128(void* p, const V4& v) {
 
 // Programmatic dependent launch (sm_90+): `pdl_trigger` lets the next kernel of the stream start its CTAs while
 // this one finishes its last wave; `pdl_wait` blocks until the previous kernel has completed and its memory is
-// visible.  Every kernel below waits before its first dependent load or any store; only loads of the caller's
-// micro-gradient may precede it (its writer is the caller's own kernel, which does not trigger early, so it
-// completed before our chain could start).  Without the launch attribute both are no-ops.
+// visible.  Every kernel below waits before its first global load or store -- the caller's micro-gradient
+// included, since the kernel that wrote it may itself trigger early.  Without the launch attribute both are no-ops.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -225,11 +224,12 @@ __global__ void __launch_bounds__(256, SMPU_K1_MINB) k1_accumulate_1(uint16_t* _
     const int64_t vend = vbeg + nvec * 16;
     uint32_t bad = 0, mx = 0;
     pdl_trigger();
-    V8 g0;
-    if (tid < nvec) g0 = ld256_ro(gb + vbeg + tid * 16);   // the caller's gradient: no kernel of ours writes it
+    // Nothing is loaded before the wait, not even the caller's gradient: its writer may be a PDL-aware kernel
+    // (a CUTLASS / cuBLASLt GEMM) that lets this kernel start before its epilogue stores land.
     pdl_wait();
     if (tid < nvec) {
         const int64_t i0 = vbeg + tid * 16;
+        V8 g0 = ld256_ro(gb + i0);
         if (!FIRST) {
             V8 a0 = ld256(acc + i0);
 #pragma unroll

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.cuh"
@@ -92,7 +93,11 @@ struct smpu_ctx {
     int grid_ar = 0;
     bool ar_vec32 = false;                                  // 256-bit peer accesses in the fused all-reduce
     bool ar_mcast = false;                                  // all-gather by NVLS multicast stores
-    int ar_unroll = 1, ar_threads = 256;                    // fused all-reduce shape (tuning knobs)
+    int ar_unroll = 1, ar_threads = 256;                    // fused all-reduce shape (smpu_config.ar_*)
+    smpu_group* group = nullptr;                            // virtual rank of a one-GPU group (smpu_group_init)
+    bool w16_in_win = false;                                // w16 is a slice of the window allocation
+    cudaStream_t step_stream = nullptr;                     // group, sharded: the stream of the deferred tail
+    cudaEvent_t tail_ev = nullptr;                          // group: end of this rank's part of the update
     size_t dec_area_off = 0;
     bool sharded = false;                                   // SURVEY f2 variant (smpu_config.sharded)
     size_t w16_off = 0;                                     // w16 inside the symmetric window
@@ -124,6 +129,7 @@ struct smpu_ctx {
     int64_t* tok_dev = nullptr;        // this update's local token count, written before each replay
     int64_t* tok_host = nullptr;       // pinned ring of kRing slots feeding tok_dev
     int64_t attempts = 0;
+    int64_t first_attempt = 1;         // smpu_result serves attempts >= this (reset by set_state(SCALARS))
     bool poisoned = false;
 
     int grid_k1 = 0, grid_k2 = 0, grid_k1s = 0;
@@ -141,6 +147,23 @@ struct smpu_ctx {
     std::vector<TraceRec> trace;
     int64_t launches[SMPU_N_KERNELS] = {};
     int64_t graph_launches[SMPU_N_KERNELS] = {};   // kernels per replay of the captured update, by kind
+};
+
+// W virtual ranks on one GPU (smpu_group_init): W member ctxs, each with its own state and window, driven by one
+// host thread.  The peer kernels of lsa_allreduce.cuh run over LocalPeers; a collective step is issued when the
+// last member reaches it (the members' own stream events order it), so the host may interleave the ranks' calls in
+// any order that a real W-process job could make.
+struct smpu_group {
+    int world = 0, dev = 0;
+    std::vector<smpu_ctx*> m;
+    cudaStream_t comm = nullptr, dec = nullptr;    // bucket all-reduces; decision exchanges
+    cudaEvent_t late_ev = nullptr;
+    std::vector<int> arrived;                      // per bucket: members whose last-micro-batch bucket is accumulated
+    int next_issue = 0;                            // next bucket all-reduce, canonical order
+    int dec_arrived = 0;                           // members whose last micro-batch is complete
+    std::vector<char> stepped;                     // members that called smpu_step in the open round
+    int n_stepped = 0;
+    int per_rank = 1;                              // CTAs per virtual rank of the one-launch all-reduce
 };
 
 namespace {
@@ -314,22 +337,39 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
     return SMPU_OK;
 }
 
+LsaPeers lsa_peers(const smpu_ctx* ctx) { return LsaPeers{ctx->devcomm, ctx->win}; }
+
+// rank p's window = member p's window allocation; per_rank > 0: one launch for every rank, else one for `fixed`
+LocalPeers local_peers(const smpu_group* g, int per_rank, int fixed) {
+    LocalPeers pe{};
+    for (int p = 0; p < g->world; ++p) pe.base[p] = (char*)g->m[p]->acc;
+    pe.per_rank = per_rank;
+    pe.fixed = fixed;
+    return pe;
+}
+
 // Adam on this rank's shard ranges of bucket b (sharded variant); one-shot grid, or a small persistent grid for
 // the (normally empty) late fallback
-smpu_status launch_k2_shard(smpu_ctx* ctx, int b, int32_t need, cudaStream_t s) {
+template <class Peers>
+smpu_status launch_k2_shard_with(smpu_ctx* ctx, const Peers& pe, int b, int32_t need, cudaStream_t s) {
     int launched = 0;   // the caller's Timed counts one launch; rank 0 may add its unaligned head / tail
     for (auto& rg : ctx->shard[b]) {
         if (rg.second <= rg.first) continue;
         if (launched++) ctx->launches[SMPU_K2]++;
         int grid = grid_for((rg.second - rg.first + 7) / 8, need == DEC_APPLY_LATE ? ctx->grid_k1s : 0x7fffffff);
-#define SMPU_K2S(WW)                                                                                            \
-    k2_adam_shard<WW><<<grid, 256, 0, s>>>(ctx->win, ctx->w16_off, ctx->theta, ctx->m, ctx->v, ctx->acc, rg.first, \
-                                           rg.second, ctx->sc, need)
+#define SMPU_K2S(WW)                                                                                              \
+    k2_adam_shard<WW, Peers><<<grid, 256, 0, s>>>(pe, ctx->w16_off, ctx->theta, ctx->m, ctx->v, ctx->acc, rg.first, \
+                                                  rg.second, ctx->sc, need)
         SMPU_BY_WORLD(ctx->world, SMPU_K2S, "sharded Adam")
 #undef SMPU_K2S
         CKL("k2_adam_shard");
     }
     return SMPU_OK;
+}
+
+smpu_status launch_k2_shard(smpu_ctx* ctx, int b, int32_t need, cudaStream_t s) {
+    if (ctx->group) return launch_k2_shard_with(ctx, local_peers(ctx->group, 0, ctx->rank), b, need, s);
+    return launch_k2_shard_with(ctx, lsa_peers(ctx), b, need, s);
 }
 
 smpu_status launch_k2(smpu_ctx* ctx, int64_t lo, int64_t hi, int32_t need, cudaStream_t s) {
@@ -483,19 +523,23 @@ smpu_status accumulate_range(smpu_ctx* ctx, const uint16_t* src, int64_t lo, int
     });
 }
 
-smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t cs) {
-    const int g = ctx->grid_ar, t = ctx->ar_threads;
-    const ncclDevComm& dc = ctx->devcomm;
-    ncclWindow_t win = ctx->win;
-#define SMPU_RS(WW) k_rs_lsa<WW><<<g, 256, 0, cs>>>(dc, win, lo, hi)
-#define SMPU_MC(WW) k_ar_lsa32<WW, true><<<g, 256, 0, cs>>>(dc, win, lo, hi)
-#define SMPU_U2(WW) k_ar_lsa32<WW, false, 2><<<g, t, 0, cs>>>(dc, win, lo, hi)
-#define SMPU_V32(WW) k_ar_lsa32<WW><<<g, t, 0, cs>>>(dc, win, lo, hi)
-#define SMPU_V16(WW) k_ar_lsa<WW><<<g, 256, 0, cs>>>(dc, win, lo, hi)
+// one bucket's fused all-reduce (or reduce-scatter, sharded) with the ctx's shape; `grid` CTAs in all
+template <class Peers>
+smpu_status launch_ar_with(smpu_ctx* ctx, const Peers& pe, int grid, int64_t lo, int64_t hi, cudaStream_t cs) {
+    const int g = grid, t = ctx->ar_threads;
+#define SMPU_RS(WW) k_rs<WW, Peers><<<g, 256, 0, cs>>>(pe, lo, hi)
+#define SMPU_MC(WW) k_ar32<WW, Peers, true><<<g, 256, 0, cs>>>(pe, lo, hi)
+#define SMPU_U2(WW) k_ar32<WW, Peers, false, 2><<<g, t, 0, cs>>>(pe, lo, hi)
+#define SMPU_V32(WW) k_ar32<WW, Peers><<<g, t, 0, cs>>>(pe, lo, hi)
+#define SMPU_V16(WW) k_ar16<WW, Peers><<<g, 256, 0, cs>>>(pe, lo, hi)
     if (ctx->sharded) {
         SMPU_BY_WORLD(ctx->world, SMPU_RS, "fused reduce-scatter")
     } else if (ctx->ar_vec32 && ctx->ar_mcast) {
-        SMPU_BY_WORLD(ctx->world, SMPU_MC, "fused all-reduce")
+        if constexpr (std::is_same<Peers, LsaPeers>::value) {
+            SMPU_BY_WORLD(ctx->world, SMPU_MC, "fused all-reduce")
+        } else {
+            return set_err(SMPU_EINVAL, "multicast all-gather needs NVLS (LSA peers)");
+        }
     } else if (ctx->ar_vec32 && ctx->ar_unroll == 2) {
         SMPU_BY_WORLD(ctx->world, SMPU_U2, "fused all-reduce")
     } else if (ctx->ar_vec32) {
@@ -508,8 +552,12 @@ smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
 #undef SMPU_U2
 #undef SMPU_V32
 #undef SMPU_V16
-    CKL(ctx->sharded ? "k_rs_lsa" : "k_ar_lsa");
+    CKL(ctx->sharded ? "k_rs" : "k_ar");
     return SMPU_OK;
+}
+
+smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t cs) {
+    return launch_ar_with(ctx, lsa_peers(ctx), ctx->grid_ar, lo, hi, cs);
 }
 
 smpu_status launch_k1_many(smpu_ctx* ctx, const uint16_t* const* g, int count, int64_t lo, int64_t hi, bool first,
@@ -559,23 +607,122 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
     return SMPU_OK;
 }
 
+// Virtual group: the all-reduce of bucket b waits for every member's last-micro-batch K1 of b (their ready events)
+// and is ONE launch over every rank's window (LocalPeers); it completes every member's ar_done[b].  Issued by the
+// member whose call makes bucket b complete, in canonical bucket order.
+smpu_status group_issue_buckets(smpu_ctx* ctx) {
+    smpu_group* g = ctx->group;
+    while (g->next_issue < ctx->nb && g->arrived[g->next_issue] == g->world) {
+        const int b = g->next_issue;
+        for (smpu_ctx* q : g->m) CK(cudaStreamWaitEvent(g->comm, q->ready[b], 0));
+        smpu_status st = launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world, ctx->bbegin[b],
+                                        ctx->bbegin[b + 1], g->comm);
+        if (st != SMPU_OK) return st;
+        for (smpu_ctx* q : g->m) {
+            q->launches[SMPU_ALLREDUCE]++;
+            CK(cudaEventRecord(q->ar_done[b], g->comm));
+        }
+        g->arrived[b] = 0;
+        g->next_issue++;
+    }
+    if (g->next_issue == ctx->nb) {
+        for (smpu_ctx* q : g->m) CK(cudaEventRecord(q->comm_done, g->comm));
+        g->next_issue = 0;
+    }
+    return SMPU_OK;
+}
+
+// bucket b of the last micro-batch (W > 1) is accumulated on `s`: hand it to the all-reduce
+smpu_status bucket_ready(smpu_ctx* ctx, int b, cudaStream_t s) {
+    ctx->bucket_done[b] = 1;
+    CK(cudaEventRecord(ctx->ready[b], s));
+    if (ctx->group) {
+        ctx->group->arrived[b]++;
+        return group_issue_buckets(ctx);
+    }
+    return issue_ready_buckets(ctx);
+}
+
+DecArgs dec_args(const smpu_ctx* q) {
+    DecArgs a{};
+    a.stat = q->stat;
+    a.local_tokens = q->local_tokens;
+    a.tok_ptr = tok_src(q);
+    a.xs = q->xs;
+    a.flag = q->flag;
+    a.st = q->st;
+    a.sc = q->sc;
+    a.loss_scale = q->scale;
+    a.ring = q->ring_dev;
+    return a;
+}
+
 // W > 1, once every bucket of the last micro-batch is accumulated: the exact early overflow decision
-// (k0_early_lsa through peer memory, or k0_early after a 16-byte NCCL all-reduce on a second communicator),
+// (k0_early_x through peer memory, or k0_early after a 16-byte NCCL all-reduce on a second communicator),
 // then Adam per bucket on its own stream, each bucket right behind its gradient all-reduce -- K2 overlaps the
 // remaining all-reduces.
 smpu_status launch_decision_lsa(smpu_ctx* ctx, cudaStream_t ds) {
-#define SMPU_DEC(WW)                                                                                             \
-    k0_early_lsa<WW><<<1, 32, 0, ds>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->stat,                     \
-                                       ctx->local_tokens, tok_src(ctx), ctx->xs, ctx->st, ctx->sc, ctx->scale,   \
-                                       ctx->ring_dev, kRing - 1, ctx->dcfg, (uint32_t)ctx->grid_ar)
+    DecArgsW A{};
+    A.r[ctx->rank] = dec_args(ctx);
+    const LsaPeers pe = lsa_peers(ctx);
+#define SMPU_DEC(WW)                                                                                            \
+    k0_early_x<WW, LsaPeers, kBoth><<<1, 32, 0, ds>>>(pe, ctx->dec_area_off, A, kRing - 1, ctx->dcfg,          \
+                                                      (uint32_t)ctx->grid_ar)
     SMPU_BY_WORLD(ctx->world, SMPU_DEC, "fused decision")
 #undef SMPU_DEC
-    CKL("k0_early_lsa");
+    CKL("k0_early_x");
+    return SMPU_OK;
+}
+
+// Adam per bucket on the ctx's K2 stream, each bucket behind its all-reduce and the decision (dec_ev)
+smpu_status enqueue_adam(smpu_ctx* ctx) {
+    cudaStream_t ks = ctx->k2_stream;
+    CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
+    for (int b = 0; b < ctx->nb; ++b) {
+        int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
+        CK(cudaStreamWaitEvent(ks, ctx->ar_done[b], 0));
+        Timed t(ctx, SMPU_K2, ks);
+        smpu_status st = ctx->sharded ? launch_k2_shard(ctx, b, DEC_APPLY, ks) : launch_k2(ctx, lo, hi, DEC_APPLY, ks);
+        if (st != SMPU_OK) return st;
+    }
+    CK(cudaEventRecord(ctx->k2_done, ks));
+    return SMPU_OK;
+}
+
+// Virtual group: once the last member's last micro-batch is in, the decision exchange of every rank as two launches
+// (publish every rank's slot, then every rank reads and decides: the launch boundary is the barrier), then each
+// member's per-bucket Adam.
+smpu_status group_decision(smpu_ctx* ctx) {
+    smpu_group* g = ctx->group;
+    if (++g->dec_arrived < g->world) return SMPU_OK;
+    g->dec_arrived = 0;
+    DecArgsW A{};
+    for (smpu_ctx* q : g->m) {
+        for (int b = 0; b < q->nb; ++b) CK(cudaStreamWaitEvent(g->dec, q->ready[b], 0));
+        A.r[q->rank] = dec_args(q);
+    }
+    const LocalPeers pe = local_peers(g, 1, 0);
+    const int W = g->world;
+#define SMPU_DEC(WW)                                                                                              \
+    k0_early_x<WW, LocalPeers, kPublish><<<W, 32, 0, g->dec>>>(pe, ctx->dec_area_off, A, kRing - 1, ctx->dcfg, 0); \
+    k0_early_x<WW, LocalPeers, kDecide><<<W, 32, 0, g->dec>>>(pe, ctx->dec_area_off, A, kRing - 1, ctx->dcfg, 0)
+    SMPU_BY_WORLD(W, SMPU_DEC, "virtual decision")
+#undef SMPU_DEC
+    CKL("k0_early_x (virtual)");
+    for (smpu_ctx* q : g->m) {
+        q->launches[SMPU_DECISION_AR]++;
+        CK(cudaEventRecord(q->dec_ev, g->dec));
+    }
+    for (smpu_ctx* q : g->m) {
+        smpu_status st = enqueue_adam(q);
+        if (st != SMPU_OK) return st;
+    }
     return SMPU_OK;
 }
 
 smpu_status issue_decision(smpu_ctx* ctx) {
-    cudaStream_t ds = ctx->dec_stream, ks = ctx->k2_stream;
+    if (ctx->group) return group_decision(ctx);
+    cudaStream_t ds = ctx->dec_stream;
     for (int b = 0; b < ctx->nb; ++b) CK(cudaStreamWaitEvent(ds, ctx->ready[b], 0));
     if (ctx->ar_impl == SMPU_AR_FUSED) {
         Timed t(ctx, SMPU_DECISION_AR, ds);
@@ -598,15 +745,86 @@ smpu_status issue_decision(smpu_ctx* ctx) {
         }
     }
     CK(cudaEventRecord(ctx->dec_ev, ds));
-    CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
-    for (int b = 0; b < ctx->nb; ++b) {
-        int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
-        CK(cudaStreamWaitEvent(ks, ctx->ar_done[b], 0));
-        Timed t(ctx, SMPU_K2, ks);
-        smpu_status st = ctx->sharded ? launch_k2_shard(ctx, b, DEC_APPLY, ks) : launch_k2(ctx, lo, hi, DEC_APPLY, ks);
+    return enqueue_adam(ctx);
+}
+
+// ---------------------------------------------------------------------------------------- virtual group steps
+// A member may step once every member has given its c micro-batches (all collectives of the update are then
+// issued); in the sharded layout its result exists only once the last member steps, so out must be NULL before.
+smpu_status group_step_check(const smpu_ctx* ctx, const smpu_step_result* out) {
+    const smpu_group* g = ctx->group;
+    for (const smpu_ctx* q : g->m)
+        if (!g->stepped[q->rank] && (q->micro != q->cfg.update_freq || q->bucket_micro))
+            return set_err(SMPU_ESTATE, "virtual group: every rank gives its %d micro-batches before any rank steps "
+                                        "(rank %d has %d)", q->cfg.update_freq, q->rank, q->micro);
+    if (ctx->sharded && out && g->n_stepped + 1 < g->world)
+        return set_err(SMPU_ESTATE, "virtual group, sharded: the update completes when the last rank steps; pass "
+                                    "out = NULL and read smpu_result afterwards");
+    return SMPU_OK;
+}
+
+void group_mark_stepped(smpu_ctx* ctx) {
+    smpu_group* g = ctx->group;
+    g->stepped[ctx->rank] = 1;
+    if (++g->n_stepped == g->world) {            // the round is closed: every rank may start its next update
+        std::fill(g->stepped.begin(), g->stepped.end(), 0);
+        g->n_stepped = 0;
+    }
+}
+
+smpu_status group_round_open_for(const smpu_ctx* ctx) {
+    if (ctx->group && ctx->group->stepped[ctx->rank])
+        return set_err(SMPU_ESTATE, "virtual group: rank %d stepped; the other ranks step before its next update",
+                       ctx->rank);
+    return SMPU_OK;
+}
+
+// Sharded layout, virtual group: this member's shard sweep is enqueued on s; the rest of the update (late flag
+// exchange, late Adam, the end-of-update barrier) runs for every member once the last one steps.
+smpu_status group_sharded_tail(smpu_ctx* ctx, cudaStream_t s) {
+    smpu_group* g = ctx->group;
+    CK(cudaEventRecord(ctx->tail_ev, s));
+    ctx->step_stream = s;
+    ctx->micro = 0;
+    ctx->local_tokens = 0;
+    std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    g->stepped[ctx->rank] = 1;
+    if (++g->n_stepped < g->world) return SMPU_OK;
+    DecArgsW A{};
+    for (smpu_ctx* q : g->m) {
+        CK(cudaStreamWaitEvent(g->dec, q->tail_ev, 0));
+        A.r[q->rank] = dec_args(q);
+    }
+    const LocalPeers pe = local_peers(g, 1, 0);
+    const int W = g->world;
+#define SMPU_KL(WW)                                                                                               \
+    k0_late_x<WW, LocalPeers, kPublish><<<W, 32, 0, g->dec>>>(pe, ctx->dec_area_off, A, kRing - 1, ctx->dcfg, 0); \
+    k0_late_x<WW, LocalPeers, kDecide><<<W, 32, 0, g->dec>>>(pe, ctx->dec_area_off, A, kRing - 1, ctx->dcfg, 0)
+    SMPU_BY_WORLD(W, SMPU_KL, "virtual late decision")
+#undef SMPU_KL
+    CKL("k0_late_x (virtual)");
+    CK(cudaEventRecord(g->late_ev, g->dec));
+    for (smpu_ctx* q : g->m) {
+        q->launches[SMPU_K0]++;
+        CK(cudaStreamWaitEvent(q->step_stream, g->late_ev, 0));
+        for (int b = 0; b < q->nb; ++b) {
+            q->launches[SMPU_K2]++;
+            smpu_status st = launch_k2_shard(q, b, DEC_APPLY_LATE, q->step_stream);
+            if (st != SMPU_OK) return st;
+        }
+        CK(cudaEventRecord(q->tail_ev, q->step_stream));
+    }
+    // end-of-update barrier: every member's next update waits for every member's w16 stores and window reads
+    for (smpu_ctx* q : g->m)
+        for (smpu_ctx* p : g->m) CK(cudaStreamWaitEvent(q->step_stream, p->tail_ev, 0));
+    for (smpu_ctx* q : g->m) {
+        q->attempts++;
+        CK(cudaEventRecord(q->ring_ev[(q->attempts - 1) % kRing], q->step_stream));
+        smpu_status st = leave_stream(q, q->step_stream);
         if (st != SMPU_OK) return st;
     }
-    CK(cudaEventRecord(ctx->k2_done, ks));
+    std::fill(g->stepped.begin(), g->stepped.end(), 0);
+    g->n_stepped = 0;
     return SMPU_OK;
 }
 
@@ -669,6 +887,13 @@ smpu_status check_cfg(const smpu_config* c) {
         return set_err(SMPU_EINVAL, "need min_scale_log2 <= init_scale_log2 <= max_scale_log2 within +-120");
     if (c->growth_interval < 1) return set_err(SMPU_EINVAL, "growth_interval must be >= 1");
     if (c->bucket_bytes < 2) return set_err(SMPU_EINVAL, "bucket_bytes must be >= 2");
+    if (c->ar_ctas < 0 || (c->ar_threads != 256 && c->ar_threads != 512) ||
+        (c->ar_vec_bytes != 16 && c->ar_vec_bytes != 32) || (c->ar_unroll != 1 && c->ar_unroll != 2) ||
+        (c->ar_mcast != 0 && c->ar_mcast != 1) || (c->pdl != 0 && c->pdl != 1))
+        return set_err(SMPU_EINVAL, "bad all-reduce shape: ar_ctas >= 0, ar_threads 256|512, ar_vec_bytes 16|32, "
+                                    "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1");
+    if (c->ar_mcast && c->ar_vec_bytes != 32)
+        return set_err(SMPU_EINVAL, "ar_mcast needs ar_vec_bytes = 32");
     return SMPU_OK;
 }
 
@@ -687,7 +912,7 @@ void free_ctx(smpu_ctx* c) {
     cudaFree(c->acc32);
     cudaFree(c->m_b);
     cudaFree(c->v_b);
-    if (!c->acc_from_nccl) cudaFree(c->w16);
+    if (!c->w16_in_win) cudaFree(c->w16);
     if (c->acc_from_nccl) ncclMemFree(c->acc);
     else cudaFree(c->acc);
     cudaFree(c->flag);
@@ -704,6 +929,7 @@ void free_ctx(smpu_ctx* c) {
     for (auto& e : c->ar_done) if (e) cudaEventDestroy(e);
     if (c->dec_ev) cudaEventDestroy(c->dec_ev);
     if (c->k2_done) cudaEventDestroy(c->k2_done);
+    if (c->tail_ev) cudaEventDestroy(c->tail_ev);
     if (c->dec_stream) cudaStreamDestroy(c->dec_stream);
     if (c->k2_stream) cudaStreamDestroy(c->k2_stream);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -756,6 +982,12 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->fuse_final = 1;
     c->accum_fp32 = 0;
     c->split_tensors = 0;
+    c->ar_ctas = 0;
+    c->ar_threads = 256;
+    c->ar_vec_bytes = 32;
+    c->ar_unroll = 1;
+    c->ar_mcast = 0;
+    c->pdl = 1;
     return SMPU_OK;
 }
 
@@ -802,22 +1034,41 @@ smpu_status smpu_plan_shards(const int64_t* bucket_begin, int n_buckets, int wor
     return SMPU_OK;
 }
 
-smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
-                      int cuda_device, const int64_t* numel, int n_tensors, const float* init_params) {
-    if (!out) return set_err(SMPU_EINVAL, "null out");
-    *out = nullptr;
-    smpu_status s = check_cfg(cfg);
-    if (s != SMPU_OK) return s;
-    if (world < 1 || rank < 0 || rank >= world) return set_err(SMPU_EINVAL, "need 0 <= rank < world");
-    if (world > 1 && !nccl_id) return set_err(SMPU_EINVAL, "world > 1 needs an NCCL unique id");
-    if (!numel || n_tensors < 1 || !init_params) return set_err(SMPU_EINVAL, "null tensor list / params");
+// MIN and MAX over the ranks of v[0..k) (int64): one NCCL MAX all-reduce of [v, -v]
+static ncclResult_t agree(ncclComm_t comm, cudaStream_t st, const int64_t* v, int k, int64_t* mn, int64_t* mx) {
+    std::vector<int64_t> h(2 * k);
+    for (int i = 0; i < k; ++i) {
+        h[i] = v[i];
+        h[k + i] = -v[i];
+    }
+    int64_t* d = nullptr;
+    if (cudaMalloc(&d, 2 * k * sizeof(int64_t)) != cudaSuccess) return ncclUnhandledCudaError;
+    ncclResult_t r = ncclSuccess;
+    if (cudaMemcpy(d, h.data(), 2 * k * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess)
+        r = ncclUnhandledCudaError;
+    if (r == ncclSuccess) r = ncclAllReduce(d, d, (size_t)(2 * k), ncclInt64, ncclMax, comm, st);
+    if (r == ncclSuccess && cudaStreamSynchronize(st) != cudaSuccess) r = ncclUnhandledCudaError;
+    if (r == ncclSuccess && cudaMemcpy(h.data(), d, 2 * k * sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        r = ncclUnhandledCudaError;
+    cudaFree(d);
+    for (int i = 0; i < k; ++i) {
+        mx[i] = h[i];
+        mn[i] = -h[k + i];
+    }
+    return r;
+}
 
+// One ctx: rank `rank` of `world` over NCCL (group == nullptr), or virtual rank `rank` of a one-GPU group.
+static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
+                              int cuda_device, const int64_t* numel, int n_tensors, const float* init_params,
+                              smpu_group* group) {
     smpu_ctx* ctx = new smpu_ctx();
     ctx->cfg = *cfg;
     ctx->world = world;
     ctx->rank = rank;
     ctx->dev = cuda_device;
-    s = plan(numel, n_tensors, cfg->bucket_bytes, ctx->bbegin, cfg->split_tensors != 0);
+    ctx->group = group;
+    smpu_status s = plan(numel, n_tensors, cfg->bucket_bytes, ctx->bbegin, cfg->split_tensors != 0);
     if (s != SMPU_OK) {
         delete ctx;
         return s;
@@ -858,6 +1109,11 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
                             ? set_err(SMPU_ENOMEM, "%s: out of memory", #x)            \
                             : fail_cuda(nullptr, e_, #x, __LINE__));                   \
     } while (0)
+#define IN(x, what)                                                                    \
+    do {                                                                               \
+        ncclResult_t r_ = (x);                                                         \
+        if (r_ != ncclSuccess) return bail(fail_nccl(nullptr, r_, what, __LINE__));    \
+    } while (0)
 
     IK(cudaSetDevice(cuda_device));
     cudaDeviceProp prop;
@@ -878,25 +1134,25 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
 
     const size_t acc_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
-    // the symmetric window also carries the decision area: 2 parities x world x 16 B
     const size_t w16_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
-    // window = [acc | w16 | decision area (early + late exchange slots)]
+    // window = [acc | w16 | decision area (early + late exchange slots: 2 parities x 8 ranks x 16 B each)]
     const size_t win_bytes = acc_bytes + w16_bytes + NCCL_WIN_REQUIRED_ALIGNMENT;
     ctx->w16_off = acc_bytes;
     ctx->dec_area_off = acc_bytes + w16_bytes;
     if (cfg->sharded && world > 1 && cfg->allreduce == SMPU_AR_NCCL)
         return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce"));
-    if (world > 1 && cfg->allreduce != SMPU_AR_NCCL && world <= kMaxLsaRanks &&
-        ncclMemAlloc((void**)&ctx->acc, win_bytes) == ncclSuccess) {
+    if (group) {
+        IK(cudaMalloc(&ctx->acc, win_bytes));            // a virtual rank's window: plain device memory
+        ctx->w16_in_win = true;
+    } else if (world > 1 && cfg->allreduce != SMPU_AR_NCCL && world <= kMaxLsaRanks &&
+               ncclMemAlloc((void**)&ctx->acc, win_bytes) == ncclSuccess) {
         ctx->acc_from_nccl = true;
+        ctx->w16_in_win = true;
     } else {
-        if (cfg->allreduce == SMPU_AR_FUSED && world > 1)
-            return bail(set_err(SMPU_EINVAL, "fused all-reduce requested but ncclMemAlloc failed or world > %d",
-                                kMaxLsaRanks));
         IK(cudaMalloc(&ctx->acc, acc_bytes));
     }
-    if (ctx->acc_from_nccl) ctx->w16 = (uint16_t*)((char*)ctx->acc + ctx->w16_off);
+    if (ctx->w16_in_win) ctx->w16 = (uint16_t*)((char*)ctx->acc + ctx->w16_off);
     else IK(cudaMalloc(&ctx->w16, n * 2));
     IK(cudaMalloc(&ctx->flag, sizeof(int)));
     IK(cudaMalloc(&ctx->stat, sizeof(uint32_t)));
@@ -918,6 +1174,7 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     for (auto& e : ctx->ar_done) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->dec_ev, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->k2_done, cudaEventDisableTiming));
+    IK(cudaEventCreateWithFlags(&ctx->tail_ev, cudaEventDisableTiming));
     ctx->bucket_done.assign(ctx->nb, 0);
     IK(cudaEventCreateWithFlags(&ctx->comm_done, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming));
@@ -939,12 +1196,16 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     ctx->k1_oneshot = ctx->grid_k1 == 0x7fffffff;
     ctx->grid_k2 = grid_cap("SMPU_K2_CTAS_PER_SM", prop.multiProcessorCount, 0);
     ctx->k2_oneshot = ctx->grid_k2 == 0x7fffffff;
-    {
-        const char* pv = getenv("SMPU_PDL");
-        ctx->pdl = world == 1 && (pv ? atoi(pv) != 0 : true);
-    }
+    ctx->pdl = world == 1 && cfg->pdl != 0;
     IK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1s_sweep, 256, 0));
     ctx->grid_k1s = prop.multiProcessorCount * (occ > 0 ? occ : 1);
+    // the fused all-reduce's shape (smpu_config.ar_*): one CTA per SM with 256-bit peer accesses by default,
+    // measured best at W = 2 and 4 (fewer CTAs starve NVLink, more steal issue slots and HBM from the concurrent
+    // K1 / K2)
+    ctx->grid_ar = cfg->ar_ctas > 0 ? cfg->ar_ctas : prop.multiProcessorCount;
+    ctx->ar_vec32 = cfg->ar_vec_bytes == 32;
+    ctx->ar_unroll = cfg->ar_unroll;
+    ctx->ar_threads = cfg->ar_threads;
 
     DevCfg& d = ctx->dcfg;
     d.peak_lr = cfg->peak_lr;
@@ -966,6 +1227,7 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
         IK(cudaMemsetAsync(ctx->v_b, 0, n * 4, s0));
     }
     IK(cudaMemsetAsync(ctx->acc, 0, n * 2, s0));
+    if (ctx->w16_in_win) IK(cudaMemsetAsync((char*)ctx->acc + ctx->dec_area_off, 0, win_bytes - ctx->dec_area_off, s0));
     if (ctx->acc32) IK(cudaMemsetAsync(ctx->acc32, 0, n * 4, s0));
     IK(cudaMemsetAsync(ctx->flag, 0, sizeof(int), s0));
     IK(cudaMemsetAsync(ctx->stat, 0, sizeof(uint32_t), s0));
@@ -977,78 +1239,149 @@ smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int ran
     IK(cudaMemcpyAsync(ctx->scale, &sc0, sizeof sc0, cudaMemcpyHostToDevice, s0));
     IK(cudaStreamSynchronize(s0));
 
-    if (world > 1) {
+    if (group) {
+        // every virtual rank was given the same theta_0 (the group init's broadcast); the peer kernels need no setup
+        ctx->ar_impl = SMPU_AR_FUSED;
+        ctx->sharded = cfg->sharded != 0;
+    } else if (world > 1) {
         ncclUniqueId id;
         memcpy(&id, nccl_id, sizeof id);
-        ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
-        if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclCommInitRank", __LINE__));
+        IN(ncclCommInitRank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+        // Every rank must agree on what shapes the collectives (plan, knobs) and on whether the fused path is
+        // possible, before any collective resource is created: a difference would otherwise hang some ranks in
+        // window registration or in LSA barriers the others never join.  EINVAL on every rank instead.
+        static const char* kField[] = {"update_freq", "bucket_bytes", "split_tensors", "sharded", "accum_fp32",
+                                       "allreduce", "ar_ctas", "ar_threads", "ar_vec_bytes", "ar_unroll", "ar_mcast",
+                                       "n (parameter count)", "n_buckets", "symmetric-memory allocation"};
+        const int64_t mine[] = {cfg->update_freq, cfg->bucket_bytes, cfg->split_tensors, cfg->sharded,
+                                cfg->accum_fp32, cfg->allreduce, ctx->grid_ar, cfg->ar_threads, cfg->ar_vec_bytes,
+                                cfg->ar_unroll, cfg->ar_mcast, n, ctx->nb, ctx->acc_from_nccl ? 1 : 0};
+        constexpr int K = sizeof(mine) / sizeof(mine[0]);
+        int64_t mn[K], mx[K];
+        IN(agree(ctx->comm, s0, mine, K, mn, mx), "rank agreement all-reduce");
+        for (int i = 0; i < K - 1; ++i)
+            if (mn[i] != mx[i])
+                return bail(set_err(SMPU_EINVAL, "ranks disagree on smpu_config.%s (%lld .. %lld): every rank must "
+                                                 "pass the same config and tensor list", kField[i], (long long)mn[i],
+                                    (long long)mx[i]));
+        const bool window_everywhere = mn[K - 1] == 1;
         // replicas start bitwise identical: rank 0's theta_0
-        r = ncclBroadcast(ctx->theta, ctx->theta, (size_t)n, ncclFloat32, 0, ctx->comm, s0);
-        if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclBroadcast", __LINE__));
-        r = ncclCommSplit(ctx->comm, 0, rank, &ctx->comm2, nullptr);
-        if (r != ncclSuccess) return bail(fail_nccl(nullptr, r, "ncclCommSplit", __LINE__));
+        IN(ncclBroadcast(ctx->theta, ctx->theta, (size_t)n, ncclFloat32, 0, ctx->comm, s0), "ncclBroadcast");
+        IN(ncclCommSplit(ctx->comm, 0, rank, &ctx->comm2, nullptr), "ncclCommSplit");
         ctx->ar_impl = SMPU_AR_NCCL;
-        if (ctx->acc_from_nccl) {
+        if (window_everywhere) {
             // symmetric window over the accumulator + device communicator with one LSA barrier per CTA
-            {
-                // one CTA per SM with 256-bit peer accesses: measured best at W = 2 and 4 (fewer CTAs starve
-                // NVLink, more steal issue slots and HBM from the concurrent K1 / K2); env overrides for tuning
-                const char* ea = getenv("SMPU_AR_CTAS");
-                ctx->grid_ar = ea && atoi(ea) > 0 ? atoi(ea) : prop.multiProcessorCount;
-                const char* vv = getenv("SMPU_AR_VEC32");
-                ctx->ar_vec32 = vv ? atoi(vv) != 0 : true;
-                const char* uv = getenv("SMPU_AR_UNROLL");
-                ctx->ar_unroll = uv && atoi(uv) == 2 ? 2 : 1;
-                const char* tv = getenv("SMPU_AR_THREADS");
-                ctx->ar_threads = tv && atoi(tv) == 512 ? 512 : 256;
-            }
-            r = cudaMemset((char*)ctx->acc + ctx->dec_area_off, 0, win_bytes - ctx->dec_area_off) == cudaSuccess
-                    ? ncclSuccess
-                    : ncclUnhandledCudaError;
-            if (r == ncclSuccess)
-                r = ncclCommWindowRegister(ctx->comm, ctx->acc, win_bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC);
-            if (r == ncclSuccess) {
-                ncclDevCommRequirements reqs;
-                memset(&reqs, 0, sizeof reqs);
-                // one per all-reduce CTA + early decision + late decision + end-of-update (sharded)
-                reqs.lsaBarrierCount = ctx->grid_ar + 3;
-                const char* mcv = getenv("SMPU_AR_MCAST");
-                reqs.lsaMultimem = mcv && atoi(mcv) != 0;
-                r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
-                if (r != ncclSuccess && reqs.lsaMultimem) {      // no NVLS: fall back to unicast stores
-                    reqs.lsaMultimem = false;
-                    r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
-                }
-                if (r == ncclSuccess) {
-                    ctx->have_devcomm = true;
-                    ctx->ar_mcast = reqs.lsaMultimem;
-                }
-            }
-            if (r == ncclSuccess && ctx->devcomm.lsaSize == world && ctx->devcomm.lsaRank == rank)
+            IN(ncclCommWindowRegister(ctx->comm, ctx->acc, win_bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC),
+               "ncclCommWindowRegister");
+            ncclDevCommRequirements reqs;
+            memset(&reqs, 0, sizeof reqs);
+            // one per all-reduce CTA + early decision + late decision + end-of-update (sharded)
+            reqs.lsaBarrierCount = ctx->grid_ar + 3;
+            reqs.lsaMultimem = cfg->ar_mcast != 0;
+            ncclResult_t r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
+            ctx->have_devcomm = r == ncclSuccess;
+            const int64_t ok = r == ncclSuccess && ctx->devcomm.lsaSize == world && ctx->devcomm.lsaRank == rank;
+            int64_t okmn, okmx;
+            IN(agree(ctx->comm, s0, &ok, 1, &okmn, &okmx), "rank agreement all-reduce");
+            if (okmn == 1) {
                 ctx->ar_impl = SMPU_AR_FUSED;
-            else if (cfg->allreduce == SMPU_AR_FUSED)
-                return bail(set_err(SMPU_EINVAL, "fused all-reduce unavailable (NCCL %d, lsaSize %d of %d)", (int)r,
-                                    ctx->devcomm.lsaSize, world));
-
-            ctx->sharded = cfg->sharded && ctx->ar_impl == SMPU_AR_FUSED;
-            if (ctx->sharded) {
-                // the same shard split as k_rs_lsa: 8-element units, ceil(units / W) per rank, rank 0 also
-                // owns the bucket's unaligned head and tail
-                ctx->shard.resize(ctx->nb);
-                for (int b = 0; b < ctx->nb; ++b)
-                    shard_of_bucket(ctx->bbegin[b], ctx->bbegin[b + 1], world, rank, ctx->shard[b]);
+                ctx->ar_mcast = cfg->ar_mcast != 0;
+            } else if (cfg->ar_mcast) {
+                return bail(set_err(SMPU_EINVAL, "ar_mcast: NVLS multicast unavailable on some rank (NCCL %d here)",
+                                    (int)r));
             }
-            if (cfg->sharded && !ctx->sharded)
-                return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce (unavailable)"));
         }
+        if (cfg->allreduce == SMPU_AR_FUSED && ctx->ar_impl != SMPU_AR_FUSED)
+            return bail(set_err(SMPU_EINVAL, "fused all-reduce requested but unavailable on some rank (needs every "
+                                             "rank an NVLink load/store peer, world <= %d)", kMaxLsaRanks));
+        ctx->sharded = cfg->sharded && ctx->ar_impl == SMPU_AR_FUSED;
+        if (cfg->sharded && !ctx->sharded)
+            return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce (unavailable)"));
+    }
+    if (ctx->sharded) {
+        // the same shard split as k_rs: 8-element units, ceil(units / W) per rank, rank 0 also owns the bucket's
+        // unaligned head and tail
+        ctx->shard.resize(ctx->nb);
+        for (int b = 0; b < ctx->nb; ++b)
+            shard_of_bucket(ctx->bbegin[b], ctx->bbegin[b + 1], world, rank, ctx->shard[b]);
     }
     kc_cast<<<grid_for(n, ctx->grid_k2), 256, 0, s0>>>(ctx->theta, ctx->w16, n);
     ctx->launches[SMPU_KCAST]++;
     IK(cudaGetLastError());
     IK(cudaStreamSynchronize(s0));
 #undef IK
+#undef IN
     *out = ctx;
     return SMPU_OK;
+}
+
+smpu_status smpu_init(smpu_ctx** out, const smpu_config* cfg, int world, int rank, const void* nccl_id,
+                      int cuda_device, const int64_t* numel, int n_tensors, const float* init_params) {
+    if (!out) return set_err(SMPU_EINVAL, "null out");
+    *out = nullptr;
+    smpu_status s = check_cfg(cfg);
+    if (s != SMPU_OK) return s;
+    if (world < 1 || rank < 0 || rank >= world) return set_err(SMPU_EINVAL, "need 0 <= rank < world");
+    if (world > 1 && !nccl_id) return set_err(SMPU_EINVAL, "world > 1 needs an NCCL unique id");
+    if (!numel || n_tensors < 1 || !init_params) return set_err(SMPU_EINVAL, "null tensor list / params");
+    return create_ctx(out, cfg, world, rank, nccl_id, cuda_device, numel, n_tensors, init_params, nullptr);
+}
+
+smpu_status smpu_group_init(smpu_group** out, const smpu_config* cfg, int world, int cuda_device, const int64_t* numel,
+                            int n_tensors, const float* init_params) {
+    if (!out) return set_err(SMPU_EINVAL, "null out");
+    *out = nullptr;
+    smpu_status s = check_cfg(cfg);
+    if (s != SMPU_OK) return s;
+    if (world < 2 || world > kMaxLsaRanks) return set_err(SMPU_EINVAL, "a virtual group has 2..%d ranks", kMaxLsaRanks);
+    if (cfg->allreduce == SMPU_AR_NCCL) return set_err(SMPU_EINVAL, "a virtual group runs the fused all-reduce only");
+    if (cfg->ar_mcast) return set_err(SMPU_EINVAL, "a virtual group has no NVLS multicast (ar_mcast = 0)");
+    if (!numel || n_tensors < 1 || !init_params) return set_err(SMPU_EINVAL, "null tensor list / params");
+    smpu_group* g = new smpu_group();
+    g->world = world;
+    g->dev = cuda_device;
+    smpu_ctx* ctx = nullptr;   // for CK: errors before any member exists poison nothing
+    auto bail = [&](smpu_status st) {
+        std::string keep = g_err;
+        smpu_group_destroy(g);
+        g_err = keep;
+        return st;
+    };
+    if (cudaSetDevice(cuda_device) != cudaSuccess) return bail(set_err(SMPU_EINVAL, "bad device %d", cuda_device));
+    int lo_prio = 0, hi_prio = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&g->comm, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&g->dec, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->late_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(fail_cuda(ctx, e, "virtual group streams", __LINE__));
+    for (int r = 0; r < world; ++r) {
+        smpu_ctx* m = nullptr;
+        s = create_ctx(&m, cfg, world, r, nullptr, cuda_device, numel, n_tensors, init_params, g);
+        if (s != SMPU_OK) return bail(s);
+        g->m.push_back(m);
+    }
+    g->arrived.assign(g->m[0]->nb, 0);
+    g->stepped.assign(world, 0);
+    g->per_rank = (g->m[0]->grid_ar + world - 1) / world;
+    *out = g;
+    return SMPU_OK;
+}
+
+smpu_status smpu_group_member(smpu_group* g, int rank, smpu_ctx** out) {
+    if (!g || !out) return set_err(SMPU_EINVAL, "null argument");
+    if (rank < 0 || rank >= g->world) return set_err(SMPU_EINVAL, "rank %d out of [0, %d)", rank, g->world);
+    *out = g->m[rank];
+    return SMPU_OK;
+}
+
+void smpu_group_destroy(smpu_group* g) {
+    if (!g) return;
+    for (smpu_ctx* m : g->m) free_ctx(m);
+    cudaSetDevice(g->dev);
+    if (g->late_ev) cudaEventDestroy(g->late_ev);
+    if (g->comm) cudaStreamDestroy(g->comm);
+    if (g->dec) cudaStreamDestroy(g->dec);
+    delete g;
 }
 
 smpu_status smpu_num_params(const smpu_ctx* ctx, int64_t* n) {
@@ -1114,6 +1447,7 @@ smpu_status smpu_loss_scale(const smpu_ctx* ctx, const float** dev_scale) {
 
 smpu_status smpu_micro_begin(smpu_ctx* ctx, int64_t ntokens) {
     LIVE(ctx);
+    if (group_round_open_for(ctx) != SMPU_OK) return SMPU_ESTATE;
     if (ntokens < 0) return set_err(SMPU_EINVAL, "ntokens < 0");
     if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "previous bucket-wise micro-batch still has %d buckets", ctx->buckets_left);
     if (ctx->micro >= ctx->cfg.update_freq)
@@ -1165,11 +1499,11 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
     st = accumulate_range(ctx, (const uint16_t*)grads, ctx->bbegin[bucket], ctx->bbegin[bucket + 1], first,
                           last && ctx->world == 1 && !ctx->fused, s, multi, last && ctx->fused, last);
     if (st != SMPU_OK) return st;
-    ctx->bucket_done[bucket] = 1;
     if (multi) {
-        CK(cudaEventRecord(ctx->ready[bucket], s));
-        st = issue_ready_buckets(ctx);
+        st = bucket_ready(ctx, bucket, s);
         if (st != SMPU_OK) return st;
+    } else {
+        ctx->bucket_done[bucket] = 1;
     }
     st = leave_stream(ctx, s);
     if (st != SMPU_OK) return st;
@@ -1182,6 +1516,7 @@ smpu_status smpu_accumulate_bucket(smpu_ctx* ctx, int bucket, const void* grads,
 
 smpu_status smpu_accumulate(smpu_ctx* ctx, const void* grads, int64_t ntokens, void* stream) {
     LIVE(ctx);
+    if (group_round_open_for(ctx) != SMPU_OK) return SMPU_ESTATE;
     if (ntokens < 0) return set_err(SMPU_EINVAL, "ntokens < 0");
     if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "a bucket-wise micro-batch is open");
     if (ctx->micro >= ctx->cfg.update_freq)
@@ -1216,6 +1551,7 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const 
                                  void* stream) {
     LIVE(ctx);
     if (!grads || !ntokens || count < 1 || count > kMaxMany) return set_err(SMPU_EINVAL, "need 1..%d buffers", kMaxMany);
+    if (group_round_open_for(ctx) != SMPU_OK) return SMPU_ESTATE;
     if (ctx->bucket_micro) return set_err(SMPU_ESTATE, "a bucket-wise micro-batch is open");
     if (ctx->micro + count > ctx->cfg.update_freq)
         return set_err(SMPU_ESTATE, "%d + %d micro-batches exceed update_freq %d", ctx->micro, count,
@@ -1246,9 +1582,7 @@ smpu_status smpu_accumulate_many(smpu_ctx* ctx, const void* const* grads, const 
         for (int b = 0; b < ctx->nb; ++b) {
             st = launch_k1_many(ctx, g, count, ctx->bbegin[b], ctx->bbegin[b + 1], first, false, true, s);
             if (st != SMPU_OK) return st;
-            ctx->bucket_done[b] = 1;
-            CK(cudaEventRecord(ctx->ready[b], s));
-            st = issue_ready_buckets(ctx);
+            st = bucket_ready(ctx, b, s);
             if (st != SMPU_OK) return st;
         }
         st = leave_stream(ctx, s);
@@ -1266,6 +1600,7 @@ smpu_status smpu_allreduce_accumulator(smpu_ctx* ctx, void* stream) {
     if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_allreduce_accumulator inside an update");
     if (ctx->world == 1) return SMPU_OK;
     if (ctx->sharded) return set_err(SMPU_EINVAL, "the sharded ctx reduce-scatters; no all-reduce to run");
+    if (ctx->group) return set_err(SMPU_EINVAL, "virtual group members all-reduce inside updates only");
     CK(cudaSetDevice(ctx->dev));
     cudaStream_t s = (cudaStream_t)stream;
     smpu_status st = enter_stream(ctx, s);
@@ -1286,7 +1621,7 @@ smpu_status smpu_allreduce_accumulator(smpu_ctx* ctx, void* stream) {
 smpu_status smpu_result(smpu_ctx* ctx, int64_t attempt, smpu_step_result* out) {
     LIVE(ctx);
     if (!out) return set_err(SMPU_EINVAL, "null out");
-    if (attempt < 1 || attempt > ctx->attempts || attempt <= ctx->attempts - kRing)
+    if (attempt < ctx->first_attempt || attempt > ctx->attempts || attempt <= ctx->attempts - kRing)
         return set_err(SMPU_EINVAL, "attempt %lld not among the last %d (issued %lld)", (long long)attempt, kRing,
                        (long long)ctx->attempts);
     int slot = (int)((attempt - 1) % kRing);
@@ -1300,6 +1635,10 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     if (ctx->micro != ctx->cfg.update_freq || ctx->bucket_micro)
         return set_err(SMPU_ESTATE, "smpu_step after %d of %d micro-batches%s", ctx->micro, ctx->cfg.update_freq,
                        ctx->bucket_micro ? " (a bucket-wise micro-batch is incomplete)" : "");
+    if (ctx->group) {
+        smpu_status gs = group_step_check(ctx, out);
+        if (gs != SMPU_OK) return gs;
+    }
     CK(cudaSetDevice(ctx->dev));
     cudaStream_t s = (cudaStream_t)stream;
     smpu_status st = enter_stream(ctx, s);
@@ -1318,15 +1657,17 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
                     ctx->acc, rg.first, rg.second, ctx->flag, ctx->sc);
                 CKL("k1s_sweep");
             }
+        if (ctx->group) return group_sharded_tail(ctx, s);
         {
             Timed t(ctx, SMPU_K0, s);
+            DecArgsW A{};
+            A.r[ctx->rank] = dec_args(ctx);
+            const LsaPeers pe = lsa_peers(ctx);
             const uint32_t bi = (uint32_t)ctx->grid_ar + 1;
-#define SMPU_KL(WW)                                                                                           \
-    k0_late_lsa<WW><<<1, 32, 0, s>>>(ctx->devcomm, ctx->win, ctx->dec_area_off, ctx->flag, ctx->xs, ctx->st,  \
-                                     ctx->sc, ctx->scale, ctx->ring_dev, kRing - 1, ctx->dcfg, bi)
+#define SMPU_KL(WW) k0_late_x<WW, LsaPeers, kBoth><<<1, 32, 0, s>>>(pe, ctx->dec_area_off, A, kRing - 1, ctx->dcfg, bi)
             SMPU_BY_WORLD(ctx->world, SMPU_KL, "sharded path")
 #undef SMPU_KL
-            CKL("k0_late_lsa");
+            CKL("k0_late_x");
         }
         for (int b = 0; b < ctx->nb; ++b) {
             Timed t(ctx, SMPU_K2, s);
@@ -1335,7 +1676,7 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
         }
         {
             Timed t(ctx, SMPU_K0, s);
-            k_lsa_barrier<<<1, 32, 0, s>>>(ctx->devcomm, (uint32_t)ctx->grid_ar + 2);
+            k_lsa_barrier<<<1, 32, 0, s>>>(lsa_peers(ctx), (uint32_t)ctx->grid_ar + 2);
             CKL("k_lsa_barrier");
         }
     } else if (ctx->world > 1) {
@@ -1404,6 +1745,7 @@ smpu_status smpu_step(smpu_ctx* ctx, void* stream, smpu_step_result* out) {
     ctx->local_tokens = 0;
     ctx->next_issue = 0;
     std::fill(ctx->bucket_done.begin(), ctx->bucket_done.end(), 0);
+    if (ctx->group) group_mark_stepped(ctx);
     if (!out) return SMPU_OK;
     st = smpu_result(ctx, ctx->attempts, out);
     if (st != SMPU_OK) return st;
@@ -1416,6 +1758,7 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     if (!micro_grads || count != ctx->cfg.update_freq)
         return set_err(SMPU_EINVAL, "need update_freq = %d micro-gradient buffers", ctx->cfg.update_freq);
     if (ctx->micro != 0 || ctx->bucket_micro) return set_err(SMPU_ESTATE, "smpu_graph_capture inside an update");
+    if (ctx->group) return set_err(SMPU_EINVAL, "graph capture of a virtual group member is not supported");
     if (ctx->world > 1 && ctx->ar_impl != SMPU_AR_FUSED)
         return set_err(SMPU_EINVAL, "graph capture at world > 1 needs the fused all-reduce (SMPU_AR_FUSED): replays "
                                     "of captured NCCL collectives on two communicators hung on B200 (2 ranks)");
@@ -1440,9 +1783,12 @@ smpu_status smpu_graph_capture(smpu_ctx* ctx, const void* const* micro_grads, in
     smpu_status st = SMPU_OK;
     cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
     if (e == cudaSuccess) {
-        if (ctx->cfg.update_freq == 1 && ctx->world == 1 && ctx->k2_oneshot && !ctx->fused) {
+        if (ctx->cfg.update_freq == 1 && ctx->world == 1 && ctx->k2_oneshot && !ctx->fused &&
+            ((uintptr_t)micro_grads[0] & 31) == 0) {
             // c = 1, W = 1: R = g_1.  The buffer is fixed and read at replay, so nothing needs copying: test it
-            // for overflow in place (2 B/elem) and let Adam read it directly -- 30 instead of 32 B/elem.
+            // for overflow in place (2 B/elem) and let Adam read it directly -- 30 instead of 32 B/elem.  Only for
+            // a 32-byte aligned buffer (k1_scan / k2_adam_1 take its vectors as they do the library's own arrays);
+            // any other buffer is accumulated as usual.
             // (The accumulator, smpu_get_state(ACCUM), is then left untouched by these replays.)
             Timed t(ctx, SMPU_K1S, ctx->cap_stream);
             k1_scan<true, false><<<grid_for((ctx->n + 15) / 16, 0x7fffffff), 256, 0, ctx->cap_stream>>>(
@@ -1564,6 +1910,7 @@ smpu_status smpu_set_state(smpu_ctx* ctx, int which, const void* src, int64_t by
         float sc = ldexpf(1.0f, (int)v[0]);
         CK(cudaMemcpy(ctx->scale, &sc, sizeof sc, cudaMemcpyHostToDevice));
         ctx->attempts = v[3];
+        ctx->first_attempt = v[3] + 1;     // the ring holds no result of a restored attempt
         return SMPU_OK;
     }
     CK(cudaMemcpy(p, src, (size_t)nb, cudaMemcpyDefault));
@@ -1632,6 +1979,9 @@ smpu_status smpu_kernel_trace(smpu_ctx* ctx, int32_t* kind, int32_t* stream, dou
     return SMPU_OK;
 }
 
-void smpu_destroy(smpu_ctx* ctx) { free_ctx(ctx); }
+void smpu_destroy(smpu_ctx* ctx) {
+    if (ctx && ctx->group) return;   // a group member: smpu_group_destroy frees it
+    free_ctx(ctx);
+}
 
 }  // extern "C"

@@ -39,7 +39,9 @@ class Config(ctypes.Structure):
                 ("min_scale_log2", ctypes.c_int32), ("max_scale_log2", ctypes.c_int32),
                 ("growth_interval", ctypes.c_int64), ("update_freq", ctypes.c_int32),
                 ("bucket_bytes", ctypes.c_int64), ("allreduce", ctypes.c_int32), ("sharded", ctypes.c_int32),
-                ("fuse_final", ctypes.c_int32), ("accum_fp32", ctypes.c_int32), ("split_tensors", ctypes.c_int32)]
+                ("fuse_final", ctypes.c_int32), ("accum_fp32", ctypes.c_int32), ("split_tensors", ctypes.c_int32),
+                ("ar_ctas", ctypes.c_int32), ("ar_threads", ctypes.c_int32), ("ar_vec_bytes", ctypes.c_int32),
+                ("ar_unroll", ctypes.c_int32), ("ar_mcast", ctypes.c_int32), ("pdl", ctypes.c_int32)]
 
 
 class StepResult(ctypes.Structure):
@@ -53,6 +55,7 @@ class StepResult(ctypes.Structure):
 
 
 EXPORTS = ["smpu_abi_version", "smpu_config_default", "smpu_unique_id", "smpu_plan_buckets", "smpu_init",
+           "smpu_group_init", "smpu_group_member", "smpu_group_destroy",
            "smpu_num_params", "smpu_accumulator", "smpu_shard_ranges", "smpu_plan_shards", "smpu_allreduce_impl", "smpu_buckets",
            "smpu_weights_fp16", "smpu_loss_scale", "smpu_accumulate", "smpu_accumulate_many", "smpu_micro_begin",
            "smpu_accumulate_bucket", "smpu_tensor_ready", "smpu_step", "smpu_allreduce_accumulator", "smpu_graph_capture",
@@ -77,6 +80,9 @@ def lib():
             "smpu_unique_id": ([p, i64], st),
             "smpu_plan_buckets": ([p, i32, i64, P(ctypes.c_int), p], st),
             "smpu_init": ([P(p), P(Config), i32, i32, p, i32, p, i32, p], st),
+            "smpu_group_init": ([P(p), P(Config), i32, i32, p, i32, p], st),
+            "smpu_group_member": ([p, i32, P(p)], st),
+            "smpu_group_destroy": ([p], None),
             "smpu_num_params": ([p, P(ctypes.c_int64)], st),
             "smpu_allreduce_impl": ([p, P(ctypes.c_int)], st),
             "smpu_shard_ranges": ([p, p, i32, P(ctypes.c_int)], st),
@@ -189,13 +195,17 @@ class UpdateStep:
     """One library ctx: init(world, buckets, params) / accumulate(micro_grads, ntokens) / step() / get_master()."""
 
     def __init__(self, numel, init_params, cfg: Config | None = None, world: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None, device: int = 0):
+                 nccl_id: bytes | None = None, device: int = 0, _member=None):
         self.cfg = cfg or config_default()
-        numel = np.ascontiguousarray(numel, dtype=np.int64)
-        self._ctx = ctypes.c_void_p()
-        idbuf = ctypes.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id is not None else None
-        _check(lib().smpu_init(ctypes.byref(self._ctx), ctypes.byref(self.cfg), world, rank, idbuf, device,
-                               _ptr(numel), numel.size, _ptr(init_params)))
+        self._owned = _member is None
+        if _member is not None:          # a member of a VirtualGroup (the group owns the ctx)
+            self._ctx = _member
+        else:
+            numel = np.ascontiguousarray(numel, dtype=np.int64)
+            self._ctx = ctypes.c_void_p()
+            idbuf = ctypes.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id is not None else None
+            _check(lib().smpu_init(ctypes.byref(self._ctx), ctypes.byref(self.cfg), world, rank, idbuf, device,
+                                   _ptr(numel), numel.size, _ptr(init_params)))
         n = ctypes.c_int64()
         _check(lib().smpu_num_params(self._ctx, ctypes.byref(n)))
         self.n = n.value
@@ -335,8 +345,40 @@ class UpdateStep:
 
     def close(self):
         if self._ctx:
-            lib().smpu_destroy(self._ctx)
+            if self._owned:
+                lib().smpu_destroy(self._ctx)
             self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class VirtualGroup:
+    """smpu_group_init: `world` data-parallel ranks held on one GPU (the world > 1 kernels over local windows).
+    `members[r]` is rank r's UpdateStep; drive them like W processes would (include/smpu.h states the two rules)."""
+
+    def __init__(self, numel, init_params, cfg: Config | None = None, world: int = 2, device: int = 0):
+        self.cfg = cfg or config_default()
+        numel = np.ascontiguousarray(numel, dtype=np.int64)
+        self._g = ctypes.c_void_p()
+        _check(lib().smpu_group_init(ctypes.byref(self._g), ctypes.byref(self.cfg), world, device, _ptr(numel),
+                                     numel.size, _ptr(init_params)))
+        self.world = world
+        self.members = []
+        for r in range(world):
+            m = ctypes.c_void_p()
+            _check(lib().smpu_group_member(self._g, r, ctypes.byref(m)))
+            self.members.append(UpdateStep(numel, None, self.cfg, world=world, rank=r, device=device, _member=m))
+
+    def close(self):
+        if self._g:
+            for m in self.members:
+                m.close()
+            lib().smpu_group_destroy(self._g)
+            self._g = ctypes.c_void_p()
 
     def __del__(self):
         try:

@@ -21,8 +21,8 @@ import oracle as O  # noqa: E402
 import paper_1806_00187_b200 as P  # noqa: E402
 import synth  # noqa: E402
 from synth import models  # noqa: E402
-from tests.gpu_util import (RTOL_1, Magnitudes, check_state, decisions, gpu_state, h2t, lib_cfg,  # noqa: E402
-                            oracle_decisions, snapshot)
+from tests.gpu_util import (Magnitudes, check_state, decisions, format_report, gpu_state, h2t,  # noqa: E402
+                            lib_cfg, oracle_decisions, rtol_for, snapshot)
 
 
 class _AccView:
@@ -90,6 +90,7 @@ def main():
     mags = Magnitudes(theta0) if rank == 0 else None
     e = 7
     failures = []
+    report = []
     if use_graph:
         gbufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)]
         if not fused:      # documented limitation: graphs at W > 1 need the fused all-reduce
@@ -158,7 +159,7 @@ def main():
             before = snapshot(orc)
             ores = orc.update(grads, ntok)
             if ores["applied"]:
-                mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
+                mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta, m_before=before["m"])
             # bitwise: exactly-summable values (any order), two operands (a + b == b + a), or the fused
             # all-reduce, which sums in the oracle's ascending rank order
             if family == "exact" or world == 2 or fused:
@@ -168,7 +169,7 @@ def main():
                 if not (np.array_equal(np.isnan(R.view(np.float16)), nan) and np.array_equal(R[~nan], ores["R"][~nan])):
                     failures.append(f"update {u}: reduced gradient differs")
                 try:
-                    check_state(st, snapshot(orc), mags, RTOL_1 * 10, where=f"update {u}")
+                    check_state(st, snapshot(orc), mags, rtol_for(orc.s.t), where=f"update {u}", report=report)
                 except AssertionError as ex:
                     failures.append(str(ex))
             else:
@@ -193,6 +194,8 @@ def main():
         print("FAIL", *allf, sep="\n")
         sys.exit(1)
     if rank == 0:
+        if report:
+            print("errors:", format_report(report))
         print(f"multi-GPU parity ok: world={world} family={family} updates={updates} impl={impl} "
               f"(ran {'fused' if fused else 'nccl'}){' as CUDA graph' if use_graph else ''}"
               f"{' + sharded optimizer bitwise' if sharded else ''}{' (sharded ctx as CUDA graph)' if shard_graph else ''}{' via accumulate_many' if many else ''}"

@@ -38,12 +38,21 @@ def test_every_declared_symbol_is_exported(P):
 
 
 def test_abi_version_and_defaults(P):
-    assert P.abi_version() == 2
+    assert P.abi_version() == 3
     c = P.config_default()
     assert (c.allreduce, c.sharded, c.fuse_final, c.accum_fp32, c.split_tensors) == (0, 0, 1, 0, 0)
     assert (c.peak_lr, c.warmup_updates, c.beta1, c.beta2, c.eps) == (5e-4, 4000, 0.9, 0.98, 1e-8)  # P:104-105
     assert (c.init_scale_log2, c.min_scale_log2, c.max_scale_log2, c.growth_interval) == (7, -5, 24, 2000)  # P:158
     assert c.bucket_bytes == 150 << 20                                                                # P:212 fn
+    # the fused all-reduce's shape lives in the config (compared across ranks at init), not in the environment
+    assert (c.ar_ctas, c.ar_threads, c.ar_vec_bytes, c.ar_unroll, c.ar_mcast, c.pdl) == (0, 256, 32, 1, 0, 1)
+
+
+def test_library_reads_no_environment_knobs():
+    """Collective shape knobs come from smpu_config only (a rank with a different environment would otherwise pick
+    a different LSA barrier count or multicast requirement and hang its peers, VERDICT r1 weak #6)."""
+    src = open(os.path.join(ROOT, "paper_1806_00187_b200", "csrc", "smpu.cu")).read()
+    assert not re.findall(r'getenv\("SMPU_(AR_|PDL)', src)
 
 
 # SURVEY Appendix A.2: whole-tensor greedy buckets of Transformer-big En-De (count, last bucket MiB)
@@ -179,3 +188,19 @@ def test_shard_plan_partitions_every_bucket(P, world):
             sizes = [sum(min(h, v1) - max(l, v0) for l, h in P.smpu.plan_shards(bb[b:b + 2], world, r)
                          if min(h, v1) > max(l, v0)) // 8 for r in range(world)]
             assert sum(sizes) == units and max(sizes, default=0) <= per
+
+
+def test_config_and_group_argument_errors_need_no_gpu(P):
+    """Argument checks run before any CUDA call: a bad all-reduce shape, and virtual groups outside 2..8 ranks, with
+    the NCCL all-reduce, or with NVLS multicast, are EINVAL (include/smpu.h)."""
+    wl = models.Workload("args", [("w", 1000, 0)], 1, 1)
+    theta0 = np.zeros(1000, np.float32)
+    for bad in (dict(ar_threads=300), dict(ar_vec_bytes=8), dict(ar_unroll=3), dict(ar_ctas=-1), dict(pdl=2),
+                dict(ar_mcast=1, ar_vec_bytes=16)):
+        with pytest.raises(P.SmpuError) as ei:
+            P.UpdateStep(wl.numel, theta0, P.config_default(**bad))
+        assert ei.value.status == P.smpu.EINVAL, bad
+    for world, kw in ((1, {}), (9, {}), (2, dict(allreduce=P.smpu.AR_NCCL)), (2, dict(ar_mcast=1))):
+        with pytest.raises(P.SmpuError) as ei:
+            P.VirtualGroup(wl.numel, theta0, P.config_default(**kw), world=world)
+        assert ei.value.status == P.smpu.EINVAL, (world, kw)

@@ -35,3 +35,34 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["world"] == 2
+
+
+def test_self_launch_without_torchrun_prints_once():
+    """`bench.py --gpus 2` with no WORLD_SIZE spawns its own two ranks (127.0.0.1 rendezvous): one line, exit 0."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--config", "tiny",
+                        "--steps", "2", "--warmup", "1", "--ref-seconds", "1.5"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["world"] == 2
+
+
+def test_reference_arm_timing_fits_the_run_and_mirrors_config():
+    """ms_per_step is measured (not extrapolated): steps x ms_per_step fits inside the run's wall time; the config
+    carries the repo arm's keys (VERDICT r1 weak #3)."""
+    import time
+    t0 = time.perf_counter()
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "tiny", "--steps", "3",
+                        "--warmup", "1", "--ref-seconds", "2"], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    wall = time.perf_counter() - t0
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["steps"] * d["ms_per_step"] / 1000 < wall
+    for key in ("workload", "n_params", "n_tensors", "update_freq", "world", "bucket_mib", "n_buckets",
+                "tokens_per_update", "generator", "parallelism", "fuse_final", "accum_fp32", "path_bytes_per_elem",
+                "optimizer", "l2"):
+        assert key in d["config"], key
+    assert d["config"]["n_buckets"] == 1 and d["config"]["optimizer"] == "replicated (paper)"

@@ -66,7 +66,7 @@ def test_base_ende_full_vector(P):
         ores = orc.update([[synth.micro_grad_cpu(wl, lay, u, 0, 1, e)]], [[tok]])
         assert decisions(res) == decisions(rres) == oracle_decisions(ores)
         assert np.array_equal(ref.get_state(P.smpu.STATE_ACCUM), ores["R"])
-        mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
+        mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta, m_before=before["m"])
         got = gpu_state(step)
         check_state(got, snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
         for name, arr in gpu_state(ref).items():
@@ -114,7 +114,7 @@ def test_big_ende_sampled(P, final):
         assert np.array_equal(acc[fin], ores["R"][fin])
         assert np.array_equal(acc[~fin] & 0x7C00, ores["R"][~fin] & 0x7C00)
         if ores["applied"]:
-            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
+            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta, m_before=before["m"])
         got = gpu_state(step, idx)
         check_state(got, snapshot(orc), mags, RTOL_1 if u == 1 else 1e-5, where=f"update {u}")
         for name, arr in gpu_state(fstep, idx).items():

@@ -12,7 +12,10 @@ from hypothesis import strategies as st
 import oracle as O
 import synth
 from synth import models
-from tests.gpu_util import Magnitudes, check_state, decisions, gpu_state, h2t, lib_cfg, oracle_decisions, snapshot
+from tests.gpu_util import (Magnitudes, check_state, decisions, format_report, gpu_state, h2t, lib_cfg,
+                            oracle_decisions, rtol_for, snapshot)
+
+REPORT = []   # worst err/D over every fuzzed case (printed by the last test of the module)
 
 pytestmark = pytest.mark.gpu
 
@@ -101,6 +104,16 @@ def test_fuzz_against_oracle(case):
             fin = (R & 0x7C00) != 0x7C00
             assert np.array_equal(got[fin], R[fin]) and np.array_equal(got[~fin] & 0x7C00, R[~fin] & 0x7C00)
         if ores["applied"]:
-            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta)
-        check_state(gpu_state(step), snapshot(orc), mags, 1e-5, where=f"{case} update {u}")
+            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta, m_before=before["m"])
+        # the north star's bar: 1e-6 after the first applied update, growing by 1e-6 per update (rtol_for)
+        check_state(gpu_state(step), snapshot(orc), mags, rtol_for(orc.s.t), where=f"{case} update {u}",
+                    report=REPORT)
     step.close()
+
+
+def test_fuzz_error_report():
+    """Print the fuzzer's worst errors under R26's cumulative D and SURVEY c.4's one-step D (both asserted <= the
+    tolerance under R26 above; c.4's is reported)."""
+    if not REPORT:
+        pytest.skip("the fuzz test did not run")
+    print("fuzz worst errors:", format_report(REPORT))

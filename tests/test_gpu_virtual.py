@@ -1,0 +1,230 @@
+"""The world > 1 path on ONE GPU: W virtual ranks (smpu_group_init) against the oracle, bitwise.
+
+Every peer kernel of the multi-GPU path -- the fused bucket all-reduce, the exact early
+overflow decision exchange and the late sweep decision (readings R3/R4), the sharded reduce-scatter + Adam
++ w16 all-gather -- is the same template instantiated over local windows (csrc/lsa_allreduce.cuh,
+LocalPeers), so these tests execute the W = 2..8 arithmetic on the driver's one-GPU box: SURVEY rows a5, a6, f1, f2.
+
+Inputs: ragged tensors whose buckets (400 kB threshold) start and end off the 8/16-element vector grid, G_real
+(order-sensitive values: bitwise parity holds because the fused sum is the oracle's ascending-rank order) and
+G_exact, with every injection kind: RED_OVF (finite A_r, inf only after the sum: early decision undecided -> sweep
+-> skip), BIG (a finite 40000 after the sum: undecided -> sweep -> late apply), INF (a non-finite A_r: early
+skip), ACC_OVF (65504 + 65504 inside one rank: early skip).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from synth import models
+from tests.gpu_util import (Magnitudes, check_state, decisions, format_report, gpu_state, h2t, lib_cfg,
+                            oracle_decisions, rtol_for, snapshot, ulp16_dist)
+
+pytestmark = pytest.mark.gpu
+
+TENSORS = [("w0", 300_001, 0), ("b0", 1025, 1), ("w1", 262_144, 0), ("e", 131_072, 2), ("b1", 7, 1)]
+C = 3
+
+
+def _workload(world, family, updates):
+    inj = [dict(u=3, kind="RED_OVF", i=262_150), dict(u=4, kind="BIG", i=300_500),
+           dict(u=5, kind="INF", r=world - 1, k=2, i=17), dict(u=6, kind="ACC_OVF", r=0, i=400_000)]
+    return models.Workload("virtual", TENSORS, world, C, injections=[x for x in inj if x["u"] <= updates],
+                           family=family)
+
+
+def _same_r(got, ref, lo=0, hi=None):
+    g, r = got[lo:hi], ref[lo:hi]
+    nan = np.isnan(r.view(np.float16))
+    return np.array_equal(np.isnan(g.view(np.float16)), nan) and np.array_equal(g[~nan], r[~nan])
+
+
+def _feed(members, grads, toks, mode, rng, bb):
+    """Give every rank its c micro-batches, interleaving the ranks' calls the way `mode` says."""
+    W = len(members)
+    if mode == "calls":                      # micro-batch by micro-batch, ranks in order
+        for k in range(C):
+            for r in range(W):
+                members[r].accumulate(h2t(grads[r][k]), toks[r][k])
+    elif mode == "rank_major":               # rank by rank (the last rank's last call issues every collective)
+        for r in reversed(range(W)):
+            for k in range(C):
+                members[r].accumulate(h2t(grads[r][k]), toks[r][k])
+    elif mode == "buckets":                  # last micro-batch bucket-wise, buckets and ranks in random order
+        for k in range(C - 1):
+            for r in range(W):
+                members[r].accumulate(h2t(grads[r][k]), toks[r][k])
+        for r in range(W):
+            members[r].micro_begin(toks[r][C - 1])
+        todo = [(r, b) for r in range(W) for b in range(len(bb) - 1)]
+        rng.shuffle(todo)
+        for r, b in todo:
+            members[r].accumulate_bucket(b, h2t(grads[r][C - 1][bb[b]:bb[b + 1]]))
+    elif mode == "many":                     # resident micro-batches: the final one inside accumulate_many
+        for r in range(W):
+            members[r].accumulate(h2t(grads[r][0]), toks[r][0])
+            members[r].accumulate_many([h2t(x) for x in grads[r][1:]], toks[r][1:])
+    else:
+        raise ValueError(mode)
+
+
+def _run(world, family="real", sharded=False, mode="calls", updates=6):
+    import paper_1806_00187_b200 as P
+    wl = _workload(world, family, updates)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, bucket_bytes=400_000, sharded=int(sharded)), world=world)
+    members = grp.members
+    bb = members[0].bucket_begin
+    assert len(bb) - 1 >= 2 and any(int(x) % 16 for x in bb[1:-1]), "buckets must cut off the vector grid"
+    ranges = [m.shard_ranges() for m in members]
+    if sharded:
+        mark = np.zeros(lay.n, np.int32)
+        for rr in ranges:
+            for lo, hi in rr:
+                mark[lo:hi] += 1
+        assert (mark == 1).all(), "shards must partition the vector"
+    orc = O.Oracle(theta0)
+    mags = Magnitudes(theta0)
+    rng = np.random.default_rng(world * 131 + len(mode))
+    report, seen = [], set()
+    e = 7
+    for u in range(1, updates + 1):
+        grads = [[synth.micro_grad_cpu(wl, lay, u, r, k, e) for k in range(1, C + 1)] for r in range(world)]
+        toks = [[synth.ntokens(wl, u, r, k) for k in range(1, C + 1)] for r in range(world)]
+        _feed(members, grads, toks, mode, rng, bb)
+        for r in rng.permutation(world):
+            members[r].step(wait=False)
+        res = [m.result(u) for m in members]
+        before = snapshot(orc)
+        ores = orc.update(grads, toks)
+        seen.add((ores["overflow"], ores["applied"]))
+        for r in range(world):
+            assert decisions(res[r]) == oracle_decisions(ores), (u, r, decisions(res[r]), oracle_decisions(ores))
+        if ores["applied"]:
+            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta, m_before=before["m"])
+        # the reduced gradient R, bitwise (NaN as a class): everywhere (replicated) or on the rank's shard
+        for r in range(world):
+            acc = members[r].get_state(P.smpu.STATE_ACCUM)
+            spans = ranges[r] if sharded else [(0, lay.n)]
+            assert all(_same_r(acc, ores["R"], lo, hi) for lo, hi in spans), f"update {u} rank {r}: R differs"
+        states = [gpu_state(m) for m in members]
+        w16 = states[0]["w16"]
+        assert all(np.array_equal(s["w16"], w16) for s in states), f"update {u}: replicas' w16 differ"
+        rtol = rtol_for(orc.s.t)
+        if sharded:
+            for r in range(world):
+                idx = np.concatenate([np.arange(lo, hi) for lo, hi in ranges[r]])
+                got = {k: v[idx] for k, v in states[r].items()}
+                sub = type(mags).__new__(type(mags))
+                sub.th, sub.m, sub.th1, sub.m1 = mags.th[idx], mags.m[idx], mags.th1[idx], mags.m1[idx]
+                check_state(got, snapshot(orc, idx), sub, rtol, where=f"update {u} rank {r} shard", report=report)
+            d = ulp16_dist(w16, orc.w16)        # the all-gathered w16: every element, every replica
+            assert d.max() <= 1, f"update {u}: w16 differs by {d.max()} ulp"
+        else:
+            h = [hashlib.sha256(b"".join(s[x].tobytes() for x in ("theta", "m", "v", "w16"))).hexdigest()
+                 for s in states]
+            assert len(set(h)) == 1, f"update {u}: replicas differ"
+            check_state(states[0], snapshot(orc), mags, rtol, where=f"update {u}", report=report)
+        e = res[0]["scale_log2_next"]
+    grp.close()
+    if updates >= 6:
+        assert (1, 0) in seen and (0, 1) in seen
+    print(f"virtual W={world} {family} {'sharded' if sharded else 'replicated'} {mode}: {format_report(report)}")
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("sharded", [False, True], ids=["replicated", "sharded"])
+def test_virtual_world_bitwise(world, sharded):
+    """G_real, call by call: decisions and R bitwise, theta/m/v within c.4 (1e-6 at update 1), w16 <= 1 ulp,
+    replicas identical; through RED_OVF / BIG / INF / ACC_OVF."""
+    _run(world, "real", sharded)
+
+
+@pytest.mark.parametrize("world,sharded", [(3, False), (8, True), (5, False)])
+def test_virtual_buckets_out_of_order(world, sharded):
+    """Bucket-wise last micro-batches, buckets and ranks interleaved at random: all-reduces still issue in canonical
+    bucket order and R is unchanged."""
+    _run(world, "real", sharded, mode="buckets")
+
+
+@pytest.mark.parametrize("world,sharded", [(4, False), (7, True)])
+def test_virtual_accumulate_many(world, sharded):
+    _run(world, "real", sharded, mode="many")
+
+
+@pytest.mark.parametrize("world,sharded", [(8, False), (6, True)])
+def test_virtual_rank_major_order_exact_family(world, sharded):
+    """Rank-major calls (rank W-1 first, each rank all its micro-batches) with G_exact."""
+    _run(world, "exact", sharded, mode="rank_major")
+
+
+def test_virtual_world_invariance_w8():
+    """(W = 8, c = 1) over 8 virtual ranks == (1, c = 8) on one ctx, bit for bit with G_real (SURVEY c.3): the
+    fused all-reduce adds rank by rank exactly as one rank accumulates micro-batch by micro-batch."""
+    import paper_1806_00187_b200 as P
+    W = 8
+    wl8 = models.Workload("inv", TENSORS, W, 1, family="real")
+    wl1 = models.Workload("inv", TENSORS, 1, W, family="real")
+    lay = synth.Layout(wl8)
+    theta0 = synth.theta0_cpu(wl8, lay)
+    grp = P.VirtualGroup(wl8.numel, theta0, lib_cfg(wl8, bucket_bytes=400_000), world=W)
+    one = P.UpdateStep(wl1.numel, theta0, lib_cfg(wl1, bucket_bytes=400_000, fuse_final=0))
+    e = 7
+    for u in range(1, 4):
+        g = [synth.micro_grad_cpu(wl8, lay, u, r, 1, e) for r in range(W)]
+        t = [synth.ntokens(wl8, u, r, 1) for r in range(W)]
+        for r in range(W):
+            grp.members[r].accumulate(h2t(g[r]), t[r])
+        for k in range(W):
+            one.accumulate(h2t(g[k]), t[k])
+        for m in grp.members:
+            m.step(wait=False)
+        r1 = one.step()
+        assert decisions(grp.members[0].result(u)) == decisions(r1)
+        a, b = gpu_state(grp.members[W - 1]), gpu_state(one)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (u, k)
+        e = r1["scale_log2_next"]
+    grp.close()
+    one.close()
+
+
+def test_virtual_group_call_rules():
+    """include/smpu.h's two rules for group members, each an ESTATE that leaves the group usable; graphs refused."""
+    import paper_1806_00187_b200 as P
+    W = 3
+    wl = models.Workload("rules", [("w", 40_000, 0)], W, 2, family="real")
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    for sharded in (0, 1):
+        grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, sharded=sharded), world=W)
+        ms = grp.members
+        g = [[h2t(synth.micro_grad_cpu(wl, lay, 1, r, k, 7)) for k in (1, 2)] for r in range(W)]
+        for r in range(W):
+            ms[r].accumulate(g[r][0], 100)
+        ms[0].accumulate(g[0][1], 100)
+        with pytest.raises(P.SmpuError) as ei:     # rank 1 and 2 have not given their last micro-batch
+            ms[0].step(wait=False)
+        assert ei.value.status == P.smpu.ESTATE
+        for r in (1, 2):
+            ms[r].accumulate(g[r][1], 100)
+        if sharded:
+            with pytest.raises(P.SmpuError) as ei:  # the sharded update completes with the last rank's step
+                ms[0].step(wait=True)
+            assert ei.value.status == P.smpu.ESTATE
+        ms[0].step(wait=False)
+        with pytest.raises(P.SmpuError) as ei:     # rank 0's next update waits for the round to close
+            ms[0].accumulate(g[0][0], 100)
+        assert ei.value.status == P.smpu.ESTATE
+        ms[1].step(wait=False)
+        ms[2].step(wait=False)
+        res = [m.result(1) for m in ms]
+        assert all(x["applied"] == 1 and x["ntokens_total"] == 600 for x in res)
+        with pytest.raises(P.SmpuError) as ei:
+            ms[1].graph_capture([g[1][0], g[1][1]])
+        assert ei.value.status == P.smpu.EINVAL
+        ms[0].accumulate(g[0][0], 100)              # the round closed: next update is open
+        grp.close()
