@@ -46,8 +46,9 @@ def parse():
                          "all-gather of w16 (bitwise equal to the replicated update); auto = replicated headline "
                          "with the sharded variant timed beside it when the fused all-reduce is available")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
-    ap.add_argument("--generator", choices=["real", "exact", "zero"], default="real",
-                    help="input family (SURVEY 8(d.2)); the performance-independence check times all three")
+    ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
+                    help="input family (SURVEY 8(d.2)); real_sparse = G_real with the row-sparse embedding gradient "
+                         "(Zipf(1.1) token rows); the performance-independence check times all four")
     ap.add_argument("--accum-fp32", action="store_true",
                     help="SURVEY Z1 knob (smpu_config.accum_fp32): fp32 accumulator, rn16 of the last sum")
     ap.add_argument("--fuse-final", type=int, choices=[0, 1], default=1,
@@ -70,6 +71,14 @@ def parse():
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: oracle seconds for the whole run, spread over the steps")
     return ap.parse_args()
+
+
+def set_generator(wl, generator):
+    """--generator: the input family, and for real_sparse the row-sparse embedding (rows of d elements)."""
+    wl.family = "real" if generator == "real_sparse" else generator
+    if generator == "real_sparse":
+        wl.embed_row = {"transformer_big_ende": 1024, "transformer_big_enfr": 1024, "transformer_base_ende": 512}.get(wl.name, 64)
+    return wl
 
 
 def workload(name, world, update_freq):
@@ -210,7 +219,8 @@ def bench_config(args, wl, world, toks_per_update, path_bytes_per_elem, sharded=
         n_buckets = plan_buckets_host(wl.numel, int(args.bucket_mib * (1 << 20)))
     return {"workload": wl.name, "n_params": wl.n, "n_tensors": len(wl.numel), "update_freq": c, "world": world,
             "bucket_mib": args.bucket_mib, "n_buckets": n_buckets, "tokens_per_update": int(toks_per_update),
-            "generator": {"real": "G_real", "exact": "G_exact", "zero": "zeros"}[args.generator] + " (SURVEY 8(d.2))",
+            "generator": {"real": "G_real", "exact": "G_exact", "zero": "zeros",
+                          "real_sparse": "G_real + row-sparse embedding"}[args.generator] + " (SURVEY 8(d.2))",
             "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
             "path_bytes_per_elem": path_bytes_per_elem,
             "optimizer": "sharded (SURVEY f2)" if (sharded and world > 1) else "replicated (paper)",
@@ -235,8 +245,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    wl = workload(args.config, args.gpus, args.update_freq)
-    wl.family = args.generator
+    wl = set_generator(workload(args.config, args.gpus, args.update_freq), args.generator)
     W, c = wl.world, wl.update_freq
     # probe: one update on a small slice gives the oracle's rate; then size the slice for the budget
     probe_v, probe_s, _ = oracle_rate(wl, 0.0, slice_elems=min(wl.n, 1 << 18))
@@ -574,8 +583,7 @@ def main_ours(args):
     import paper_1806_00187_b200 as P
     import synth
 
-    wl = workload(args.config, world, args.update_freq)
-    wl.family = args.generator
+    wl = set_generator(workload(args.config, world, args.update_freq), args.generator)
     lay = synth.Layout(wl)
     c, n = wl.update_freq, lay.n
 

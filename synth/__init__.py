@@ -41,6 +41,8 @@ def _load():
         lib.synth_sample.argtypes = [p, p, i64, i32, p, p, i32, u64, i32, i32]
         lib.synth_theta0.argtypes = [p, i64, u64]
         lib.synth_theta0_sample.argtypes = [p, p, i64, u64]
+        lib.synth_embed_rows.restype = i64
+        lib.synth_embed_rows.argtypes = [p, i64, u64, i64, ctypes.c_double]
         _lib = lib
     return _lib
 
@@ -133,12 +135,45 @@ def overrides(wl: Workload, u: int, r: int, k: int):
     return out
 
 
+ZIPF_S = 1.1   # token ids ~ Zipf(1.1)
+
+
+def embed_mask(wl: Workload, n_rows: int, u: int, r: int, k: int) -> np.ndarray:
+    """Rows of an embedding tensor that carry gradient in micro-batch (u, r, k): those of its ntokens(u, r, k) token
+    ids, drawn from Zipf(1.1) over the rows (synth_embed_rows).  uint8[n_rows]; one array for both fills."""
+    mask = np.empty(n_rows, dtype=np.uint8)
+    kk = key(wl.seed, u, r, k)
+    if _load().synth_embed_rows(_ptr(mask), n_rows, kk, _load().synth_ntokens(kk), ZIPF_S) < 0:
+        raise MemoryError("synth_embed_rows")
+    return mask
+
+
+def embed_spans(wl: Workload, lay: Layout):
+    """[(lo, hi, n_rows)] of the embedding tensors when the workload's embedding gradient is row-sparse."""
+    if not wl.embed_row:
+        return []
+    return [(int(lay.begin[j]), int(lay.begin[j + 1]), -(-int(lay.begin[j + 1] - lay.begin[j]) // wl.embed_row))
+            for j in range(lay.n_tensors) if lay.cls[j] == 2]
+
+
+def _apply_rows_range(out, lo, hi, wl, lay, u, r, k):
+    """Zero out[i - lo] for i in [lo, hi) in an embedding row that holds no token of the micro-batch."""
+    for a, b, rows in embed_spans(wl, lay):
+        s0, s1 = max(a, lo), min(b, hi)
+        if s0 >= s1:
+            continue
+        mask = embed_mask(wl, rows, u, r, k)
+        keep = mask[(np.arange(s0, s1) - a) // wl.embed_row].astype(bool)
+        out[s0 - lo:s1 - lo][~keep] = 0
+
+
 def micro_grad_cpu(wl: Workload, lay: Layout, u: int, r: int, k: int, e: int, family: str | None = None):
     """Full packed fp16 micro-gradient g_{r,k} of update u (uint16 bit patterns)."""
     fam = FAMILIES[family or wl.family]
     out = np.empty(lay.n, dtype=np.uint16)
     _load().synth_fill(_ptr(out), lay.n_tensors, _ptr(lay.begin), _ptr(lay.cls), fam,
                        key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq))
+    _apply_rows_range(out, 0, lay.n, wl, lay, u, r, k)
     for i, bits in overrides(wl, u, r, k):
         out[i] = bits
     return out
@@ -151,6 +186,7 @@ def micro_grad_range(wl: Workload, lay: Layout, lo: int, hi: int, u: int, r: int
     out = np.empty(hi - lo, dtype=np.uint16)
     _load().synth_fill_range(_ptr(out), lo, hi, lay.n_tensors, _ptr(lay.begin), _ptr(lay.cls), fam,
                              key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq))
+    _apply_rows_range(out, lo, hi, wl, lay, u, r, k)
     for i, bits in overrides(wl, u, r, k):
         if lo <= i < hi:
             out[i - lo] = bits
@@ -165,6 +201,11 @@ def micro_grad_sample(wl: Workload, lay: Layout, idx: np.ndarray, u: int, r: int
     out = np.empty(idx.size, dtype=np.uint16)
     _load().synth_sample(_ptr(out), _ptr(idx), idx.size, lay.n_tensors, _ptr(lay.begin), _ptr(lay.cls), fam,
                          key(wl.seed, u, r, k), e, exact_K(wl.world, wl.update_freq))
+    for a, b, rows in embed_spans(wl, lay):
+        sel = (idx >= a) & (idx < b)
+        if sel.any():
+            mask = embed_mask(wl, rows, u, r, k)
+            out[sel] = np.where(mask[(idx[sel] - a) // wl.embed_row].astype(bool), out[sel], 0)
     pos = {int(v): j for j, v in enumerate(idx)}
     for i, bits in overrides(wl, u, r, k):
         if i in pos:
@@ -202,6 +243,15 @@ def micro_grad_gpu(out, wl: Workload, lay: Layout, u: int, r: int, k: int, e: in
                                         ctypes.c_void_p(s.cuda_stream))
     if rc != 0:
         raise RuntimeError(f"synth_gpu_fill: cuda error {rc}")
+    for a, b, rows in embed_spans(wl, lay):     # the same mask array as the CPU fill (embed_mask)
+        with torch.cuda.stream(s):
+            mask = torch.from_numpy(embed_mask(wl, rows, u, r, k).astype(bool)).to(out.device)
+            seg = out.view(torch.int16)[a:b]
+            full = (b - a) // wl.embed_row
+            if full:
+                seg[:full * wl.embed_row].view(full, wl.embed_row)[~mask[:full]] = 0
+            if full < rows and not bool(mask[rows - 1]):
+                seg[full * wl.embed_row:] = 0
     ov = overrides(wl, u, r, k)
     if ov:
         with torch.cuda.stream(s):

@@ -60,6 +60,8 @@ class Workload:
     injections: list = field(default_factory=list)
     family: str = "real"     # real | exact | zero
     updates: int = 10
+    embed_row: int = 0       # > 0: row-sparse embedding gradient with rows of this many elements;
+                             # 0: dense (reading R27: the tied output projection touches every row)
 
     @property
     def numel(self):

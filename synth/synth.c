@@ -24,6 +24,7 @@
 #include <stdint.h>
 #include <string.h>
 #include <math.h>
+#include <stdlib.h>
 
 #define SYNTH_GOLDEN 0x9e3779b97f4a7c15ULL
 
@@ -126,4 +127,33 @@ void synth_theta0(float* out, int64_t n, uint64_t key) {
 
 void synth_theta0_sample(float* out, const int64_t* idx, int64_t m, uint64_t key) {
     for (int64_t j = 0; j < m; ++j) out[j] = ldexpf((float)lanes_q(synth_mix(key ^ (uint64_t)idx[j])), -21);
+}
+
+/* Row-sparse embedding gradient: only the rows of the micro-batch's token ids carry gradient.
+ * mask[v] = 1 iff row v is among T token ids drawn i.i.d. from Zipf(s) over the V rows -- p(v) proportional to
+ * (v + 1)^-s, row 0 the most frequent -- by inverse CDF with the uniform (f(key ^ (0xE3B0 << 32) ^ t) >> 11) * 2^-53
+ * for draw t.  The mask is an input: the CPU and GPU fills both apply this one array.  Returns the distinct rows. */
+int64_t synth_embed_rows(uint8_t* mask, int64_t V, uint64_t key, int64_t T, double s) {
+    double* cdf = (double*)malloc((size_t)V * sizeof(double));
+    if (!cdf) return -1;
+    double acc = 0.0;
+    for (int64_t v = 0; v < V; ++v) {
+        acc += pow((double)(v + 1), -s);
+        cdf[v] = acc;
+    }
+    memset(mask, 0, (size_t)V);
+    int64_t distinct = 0;
+    for (int64_t t = 0; t < T; ++t) {
+        const double x = (double)(synth_mix(key ^ (0xE3B0ULL << 32) ^ (uint64_t)t) >> 11) * 0x1.0p-53 * acc;
+        int64_t lo = 0, hi = V - 1;            /* first v with cdf[v] > x */
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (cdf[mid] > x) hi = mid;
+            else lo = mid + 1;
+        }
+        distinct += !mask[lo];
+        mask[lo] = 1;
+    }
+    free(cdf);
+    return distinct;
 }

@@ -1,7 +1,7 @@
 """Randomised parity (hypothesis, fixed seed): random tensor lists (sizes 1..40k, every class), update_freq 1..5,
 bucket thresholds from a few bytes to 1 MiB, every accumulation entry point (whole / bucket-wise in a random
 order / resident accumulate_many / in-place NULL / CUDA graph), fuse_final on or off, the fp32 accumulator
-(SURVEY Z1 knob) in a quarter of the cases, injected non-finites
+(SURVEY Z1 knob) in a quarter of the cases, row-sparse embedding gradients in half, injected non-finites
 anywhere; the library vs the oracle on decisions (bitwise), the accumulator (bitwise, wherever it holds R) and
 theta/m/v/w16 (tolerance), every update."""
 import numpy as np
@@ -41,7 +41,8 @@ def cases(draw):
     order_seed = draw(st.integers(0, 1000))
     fuse = draw(st.booleans())
     acc32 = draw(st.integers(0, 3)) == 0          # the Z1 fp32-accumulator knob in a quarter of the cases
-    return tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32
+    embed_row = draw(st.sampled_from([0, 0, 16, 64]))   # row-sparse embedding gradients in half
+    return tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32, embed_row
 
 
 @seed(20261018)
@@ -50,8 +51,8 @@ def cases(draw):
 def test_fuzz_against_oracle(case):
     import torch
     import paper_1806_00187_b200 as P
-    tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32 = case
-    wl = models.Workload("fuzz", tensors, 1, c, injections=inj)
+    tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32, embed_row = case
+    wl = models.Workload("fuzz", tensors, 1, c, injections=inj, embed_row=embed_row)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
     ocfg = O.Config(accum_fp32=acc32)

@@ -36,3 +36,15 @@ def test_gpu_generator_matches_cpu_sampled_big():
     synth.micro_grad_gpu(out, wl, lay, 2, 0, 16, 7)
     got = out[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint16)
     assert np.array_equal(got, synth.micro_grad_sample(wl, lay, idx, 2, 0, 16, 7))
+
+
+def test_gpu_generator_row_sparse_embedding_matches_cpu():
+    """The row-sparse embedding option gives the same bits on both sides, partial last row too."""
+    import torch
+    wl = models.Workload("t", [("a", 70_001, 0), ("e", 4001 * 64 + 17, 2)], 2, 2, embed_row=64)
+    lay = synth.Layout(wl)
+    out = torch.empty(lay.n, dtype=torch.int16, device="cuda")
+    for (u, r, k) in [(1, 0, 1), (2, 1, 2), (7, 0, 2)]:
+        synth.micro_grad_gpu(out, wl, lay, u, r, k, 7)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint16), synth.micro_grad_cpu(wl, lay, u, r, k, 7))

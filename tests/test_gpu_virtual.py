@@ -228,3 +228,73 @@ def test_virtual_group_call_rules():
         assert ei.value.status == P.smpu.EINVAL
         ms[0].accumulate(g[0][0], 100)              # the round closed: next update is open
         grp.close()
+
+
+def test_c3_enfr_5200_updates_virtual_w8(gold):
+    """BASELINE.json configs[3] at its stated world size: Transformer-big En-Fr (221.9M params) over 8 ranks,
+    update_freq 16, 5,200 updates with the INF / NAN / ACC_OVF / RED_OVF bursts at u = 2500-2503 and 5000-5003
+     -- here as 8 virtual ranks on one GPU (28 GB of rank state).  Decisions bitwise against the
+    sampled-index oracle every update (the bounded G_exact generator cannot overflow alone, so the schedule decides,
+    SURVEY 8(d.4)), the hand-derived scaler checkpoints, sampled theta/m/v/w16 at the end (1e-4), replicas
+    bitwise identical on the device."""
+    import torch
+    import paper_1806_00187_b200 as P
+    W = 8
+    wl = models.big_enfr(world=W)
+    lay = synth.Layout(wl)
+    c = wl.update_freq
+    theta0 = torch.empty(lay.n, dtype=torch.float32, device="cuda")
+    synth.theta0_gpu(theta0, wl)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl), world=W)
+    del theta0
+    ms = grp.members
+    rng = np.random.default_rng(3)
+    bb = ms[0].bucket_begin
+    idx = np.unique(np.concatenate([rng.integers(0, lay.n, 2048), lay.begin[1:-1], bb[1:-1], bb[1:-1] - 1,
+                                    [inj["i"] for inj in wl.injections]])).astype(np.int64)
+    orc = O.Oracle(synth.theta0_sample(wl, idx))
+    mags = Magnitudes(orc.theta.copy())
+    checks = {int(r[0]): tuple(map(int, r[1:])) for r in gold("scaler_trace_c3.txt")}
+    inj_u = {inj["u"] for inj in wl.injections}
+    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(2)]
+    pending = []
+    e = 7
+    for u in range(1, wl.updates + 1):
+        j = 0
+        for k in range(1, c + 1):
+            for r in range(W):
+                synth.micro_grad_gpu(bufs[j & 1], wl, lay, u, r, k, e)
+                ms[r].accumulate(bufs[j & 1], synth.ntokens(wl, u, r, k))
+                j += 1
+        for m in ms:
+            m.step(wait=False)
+        grads = [[synth.micro_grad_sample(wl, lay, idx, u, r, k, e) for k in range(1, c + 1)] for r in range(W)]
+        toks = [[synth.ntokens(wl, u, r, k) for k in range(1, c + 1)] for r in range(W)]
+        before = snapshot(orc)
+        ores = orc.update(grads, toks, overflow=(u in inj_u))
+        if ores["applied"]:
+            mags.update(ores["R"], ores["e_used"], ores["N"], before["theta"], orc.theta, m_before=before["m"])
+        if u in checks:
+            assert (orc.e, orc.s.clean, orc.s.t) == checks[u], u
+        pending.append((u, oracle_decisions(ores)))
+        e = orc.e
+        if len(pending) >= 32 or u == wl.updates:
+            for uu, od in pending:
+                for m in ms:
+                    assert decisions(m.result(uu)) == od, (uu, m.rank)
+            pending = []
+    report = []
+    check_state(gpu_state(ms[0], idx), snapshot(orc), mags, 1e-4, where="after 5200 updates", report=report)
+    s = ms[0].scalars()
+    assert (s["e"], s["clean"], s["t"], s["attempts"]) == (1, 197, 5192, 5200)
+    for which, dt in ((P.smpu.STATE_MASTER, torch.float32), (P.smpu.STATE_M, torch.float32),
+                      (P.smpu.STATE_V, torch.float32), (P.smpu.STATE_W16, torch.int16)):
+        ref = torch.empty(lay.n, dtype=dt, device="cuda")
+        ms[0].get_state(which, out=ref)
+        other = torch.empty_like(ref)
+        for m in ms[1:]:
+            m.get_state(which, out=other)
+            assert torch.equal(ref, other), (which, m.rank)
+        del ref, other
+    grp.close()
+    print("C3 virtual W=8:", format_report(report))

@@ -80,3 +80,35 @@ def test_injection_overrides():
     with pytest.raises(ValueError):
         synth.overrides(models.Workload("x", [("a", 10, 0)], 1, 2, injections=[dict(u=1, kind="RED_OVF", i=1)]),
                         1, 0, 2)
+
+
+def test_row_sparse_embedding_zipf_rows():
+    """SURVEY 8(d.2)'s row-sparse embedding: the rows drawn for a micro-batch follow Zipf(1.1) over the vocabulary.
+    Pinned to the closed forms: E[distinct rows] = sum_v 1 - (1 - p_v)^T and P(row v drawn) = 1 - (1 - p_v)^T,
+    over many micro-batches; inactive rows are exactly zero in the fill, active ones keep G_real's values."""
+    V = 32_768
+    wl = models.Workload("emb", [("w", 4096, 0), ("e", V * 64, 2)], 1, 1, embed_row=64)
+    p = np.arange(1, V + 1, dtype=np.float64) ** -1.1
+    p /= p.sum()
+    ds, hits = [], np.zeros(V)
+    Ts = []
+    for k in range(1, 41):
+        m = synth.embed_mask(wl, V, 1, 0, k).astype(bool)
+        T = synth.ntokens(wl, 1, 0, k)
+        Ts.append(T)
+        ds.append(m.sum())
+        hits += m
+    T = np.mean(Ts)
+    expect = np.sum(1 - (1 - p) ** T)
+    assert abs(np.mean(ds) - expect) < 0.03 * expect, (np.mean(ds), expect)
+    for v in (0, 9, 99, 999):       # per-row inclusion frequency over the 40 micro-batches
+        pv = 1 - (1 - p[v]) ** T
+        assert abs(hits[v] / 40 - pv) < 4 * np.sqrt(pv * (1 - pv) / 40) + 0.02, (v, hits[v], pv)
+    lay = synth.Layout(wl)
+    g = synth.micro_grad_cpu(wl, lay, 1, 0, 1, 7)
+    dense = synth.micro_grad_cpu(models.Workload("emb", wl.tensors, 1, 1), lay, 1, 0, 1, 7)
+    rows = g[4096:].reshape(V, 64)
+    m = synth.embed_mask(wl, V, 1, 0, 1).astype(bool)
+    assert not rows[~m].any()
+    assert np.array_equal(rows[m], dense[4096:].reshape(V, 64)[m])
+    assert np.array_equal(g[:4096], dense[:4096])
