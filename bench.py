@@ -61,9 +61,15 @@ def parse():
                     help="M2 with SURVEY f3's producer: dW GEMMs accumulate in place into smpu_accumulator "
                          "(cuBLAS beta = 1; bitwise the paper's accumulate), 1-D tensors by fp16 add, no K1")
     ap.add_argument("--trace", default=None, help="write the timed launches (per stream) as JSONL here")
-    ap.add_argument("--mode", choices=["m1", "m2"], default="m1",
+    ap.add_argument("--mode", choices=["m1", "m2", "train"], default="m1",
                     help="m1: the update step alone (headline); m2: with a cuBLAS backward-load emulator so the "
-                         "bucket all-reduces overlap backward as in the paper's Fig. 3 (exposed-comm measurement)")
+                         "bucket all-reduces overlap backward as in the paper's Fig. 3 (exposed-comm measurement); "
+                         "train: the real Transformer-big forward + backward (producer/transformer.py) feeding the "
+                         "library, buckets handed over as backward finishes them (SURVEY f3; Table 1-style tok/s)")
+    ap.add_argument("--tokens", type=int, default=3500, help="train: token budget per micro-batch (P:317)")
+    ap.add_argument("--sent-len", type=int, default=28, help="train: sentence length of the synthetic batches")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="train: hand the last micro-batch over after backward (no overlap) instead of per bucket")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -445,6 +451,112 @@ def run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg,
     return out
 
 
+# ------------------------------------------------------------------------------------------ train (real producer)
+def run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, theta0):
+    """SURVEY f3 with a real producer: each micro-batch is a forward + backward of the paper's Transformer-big
+    (producer/transformer.py) on the library's fp16 weights, scaled by the library's loss scale; the first c - 1
+    micro-batches go to smpu_accumulate after their backward, the last one bucket by bucket from the backward's
+    per-tensor hooks -- or, with --no-overlap, after its backward.  Timed: whole training updates
+    (c x fwd/bwd + the update step), CUDA events, max over ranks; exposed communication against the same producer
+    through a world = 1 ctx."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "producer"))
+    from transformer import Producer, TransformerBig, device_view
+    c, n = wl.update_freq, lay.n
+    dropout = 0.1 if "enfr" in wl.name else 0.3                       # P:101
+
+    def setup(st, seed):
+        w16 = device_view(st.weights_fp16_ptr(), n, "<f2", f"cuda:{local}")
+        scale = device_view(st.loss_scale_ptr(), 1, "<f4", f"cuda:{local}")
+        model = TransformerBig(wl.tensors, w16, dropout=dropout)
+        grad = torch.empty(n, dtype=torch.float16, device=f"cuda:{local}")
+        prod = Producer(model, grad, scale, seed=seed)
+        batches = [prod.batch(args.tokens, args.sent_len) for _ in range(c)]
+        return prod, grad, batches
+
+    def bucket_of(st):
+        bb = st.bucket_begin
+        tb = [int(np.searchsorted(bb, off, side="right") - 1) for off in np.concatenate([[0], np.cumsum(wl.numel)[:-1]])]
+        per = np.bincount(tb, minlength=len(bb) - 1)
+        return tb, per, bb
+
+    def one(st, prod, grad, batches, overlap):
+        g16 = grad.view(torch.int16)
+        for k in range(c - 1):
+            src, ti, to, nt = batches[k]
+            prod.micro(src, ti, to)
+            st.accumulate(g16, nt, stream)
+        src, ti, to, nt = batches[c - 1]
+        if not overlap:
+            prod.micro(src, ti, to)
+            st.accumulate(g16, nt, stream)
+        else:
+            tb, per, bb = bucket_of(st)
+            left = per.copy()
+            st.micro_begin(nt)
+
+            def on_tensor(j):
+                b = tb[j]
+                left[b] -= 1
+                if left[b] == 0:      # the bucket's last gradient is in: hand it over now (P:211-212)
+                    st.accumulate_bucket(b, g16[int(bb[b]):int(bb[b + 1])], stream)
+            prod.micro(src, ti, to, on_tensor=on_tensor)
+        st.step(stream, wait=False)
+
+    def timed(st, w, overlap, seed):
+        prod, grad, batches = setup(st, seed)
+        for _ in range(max(1, args.warmup)):
+            one(st, prod, grad, batches, overlap)
+        torch.cuda.synchronize()
+        _barrier(w)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(local) as clk:
+            a.record(stream)
+            for _ in range(args.steps):
+                one(st, prod, grad, batches, overlap)
+            b.record(stream)
+            torch.cuda.synchronize()
+        _barrier(w)
+        last = st.result(st.scalars()["attempts"])
+        ms = a.elapsed_time(b) / args.steps
+        return _max_over_ranks(ms, w), sum(x[3] for x in batches), last, clk.summary(), prod.flops_per_token()
+
+    overlap = not args.no_overlap
+    ms, tok_rank, last, clk, fpt = timed(step, world, overlap, seed=rank)
+    ms_no = None
+    if world > 1 and overlap:
+        ms_no = timed(step, world, False, seed=rank)[0]
+    step.close()
+    ms1 = None
+    if world > 1:
+        s1 = P.UpdateStep(wl.numel, theta0, make_cfg(False, fuse_final=0), world=1, rank=0, device=local)
+        ms1 = timed(s1, 1, False, seed=rank)[0]
+        ms1 = _max_over_ranks(ms1, world)
+        s1.close()
+    tok = _sum_over_ranks(tok_rank, world)
+    if rank != 0:
+        return None
+    out = {"metric": METRIC + " (train: real Transformer-big forward/backward producer)", "mode": "train",
+           "value": world * c * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "target_tokens_per_s": tok / (ms * 1e-3), "tokens_per_update": tok, "update_freq": c,
+           "model_flops_per_token": fpt, "model_tflops_per_s_per_gpu": fpt * tok / world / (ms * 1e-3) / 1e12,
+           "last_result": {k: last[k] for k in ("applied", "overflow", "scale_log2_used", "lr", "num_updates")},
+           "overlap": "per-bucket handover from backward hooks (P:211-212)" if overlap else "after backward",
+           "config": {"workload": wl.name, "update_freq": c, "world": world, "bucket_mib": args.bucket_mib,
+                      "tokens_per_micro_budget": args.tokens, "sent_len": args.sent_len, "dropout": dropout,
+                      "label_smoothing": 0.1, "data": "synthetic uniform token ids (no dataset)",
+                      "producer": "producer/transformer.py (torch fp16 autograd on the library's w16)"},
+           "clocks": clk, "dtype": "f16+f32", "data": "synthetic"}
+    if ms1 is not None:
+        out["exposed_comm"] = {"ms": ms - ms1, "frac_of_update": (ms - ms1) / ms, "t_world1_ms": ms1,
+                               "method": "T(training update, W ranks) - T(same producer + world=1 ctx, same GPU)"}
+    if ms_no is not None:
+        out["no_overlap_ms_per_step"] = ms_no
+        out["overlap_gain"] = (ms_no - ms) / ms_no
+    return out
+
+
 # ------------------------------------------------------------------------------------------ our arm
 def _barrier(world):
     if world > 1:
@@ -622,11 +734,15 @@ def main_ours(args):
     step = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=new_id(), device=local)
     ar_impl = step.allreduce_impl
     stream = torch.cuda.current_stream()
-    if args.mode == "m2":
-        out = run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg, theta0)
+    if args.mode in ("m2", "train"):
+        if args.mode == "m2":
+            out = run_m2(args, P, wl, lay, grads, toks, step, stream, world, rank, local, cfg, theta0)
+            step.close()
+        else:
+            del grads
+            out = run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, theta0)
         if out is not None:
             print(json.dumps(out), flush=True)
-        step.close()
         if world > 1:
             dist.destroy_process_group()
         return

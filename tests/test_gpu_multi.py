@@ -169,3 +169,14 @@ def test_foreign_device_buffer_rejected():
     assert step.step()["applied"] == 1
     assert np.isfinite(step.get_master()).all()
     step.close()
+
+
+def test_mismatched_config_is_einval_on_every_rank():
+    """smpu_init compares the collective-shaping config across ranks: a mismatch is EINVAL everywhere, no hang."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", "29581", "tests/mp_mismatch_worker.py"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
+    print(p.stdout[-3000:], p.stderr[-3000:])
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
