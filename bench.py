@@ -51,9 +51,10 @@ def parse():
                          "(Zipf(1.1) token rows); the performance-independence check times all four")
     ap.add_argument("--accum-fp32", action="store_true",
                     help="SURVEY Z1 knob (smpu_config.accum_fp32): fp32 accumulator, rn16 of the last sum")
-    ap.add_argument("--fuse-final", type=int, choices=[0, 1], default=1,
-                    help="W = 1: fuse the last micro-batch's accumulation into Adam (smpu_config.fuse_final, the "
-                         "library default; 0 = accumulate, decide, then Adam)")
+    ap.add_argument("--fuse-final", type=int, choices=[0, 1], default=0,
+                    help="W = 1 headline: 0 (the library default, SURVEY 8(b)'s contract) = accumulate, decide, then "
+                         "Adam; 1 = the opt-in smpu_config.fuse_final (last micro-batch fused into Adam).  With 0 the "
+                         "fused variant is timed beside the headline")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the call-by-call path (c x smpu_accumulate + smpu_step) instead of the captured "
                          "CUDA graph of the same update (smpu_graph_capture / smpu_graph_launch)")
@@ -776,6 +777,22 @@ def main_ours(args):
     step.close()
     del step
 
+    # ---- W = 1: the opt-in fused last micro-batch (smpu_config.fuse_final = 1) beside the contract-default headline
+    fused_variant = None
+    if world == 1 and not fused and not args.accum_fp32:
+        fstep = P.UpdateStep(wl.numel, theta0, make_cfg(False, fuse_final=1), world=1, rank=0, device=local)
+        F_ = measure(args, fstep, grads, toks, stream, 1, local, resident=True)
+        fb = (4 if c > 1 else 0) + 6 * max(c - 2, 0) + (30 if c > 1 else 28)
+        k12 = F_["stats"]["k12_fused"]
+        fused_variant = {"ms_per_step": F_["ms"], "value": c * n / (F_["ms"] * 1e-3), "bytes_per_elem": fb,
+                         "path_hbm_gbs": fb * n / (F_["ms"] * 1e-3) / 1e9,
+                         "k12_achieved_gbs": (30 if c > 1 else 28) * n * k12["launches"] / max(1, k12["launches"]) /
+                                             (k12["ms"] / max(1, k12["launches"]) * 1e-3) / 1e9 if k12["ms"] > 0 else None,
+                         "resident_ms_per_step": F_.get("ms_resident"),
+                         "api": "smpu_config.fuse_final = 1 (opt-in; w16 rewritten by the last accumulate call)"}
+        fstep.close()
+        del fstep
+
     # ---- W > 1: the sharded layout beside the replicated headline, same inputs
     variant = None
     if world > 1 and not head_sharded and args.optimizer == "auto" and ar_impl == P.smpu.AR_FUSED:
@@ -883,6 +900,8 @@ def main_ours(args):
         if a:
             a["impl"] = {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)) + ("_reduce_scatter" if head_sharded else "")
             out["allreduce"] = a
+    if fused_variant:
+        out["fused_final_variant"] = fused_variant
     if variant:
         base = t1 - k2_full_ms * (1 - 1 / world)
         variant["exposed_comm_estimate"] = {

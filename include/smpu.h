@@ -71,13 +71,14 @@ typedef struct {
                                   1: sharded variant (world > 1, fused all-reduce): reduce-scatter,
                                   Adam on this rank's shard only, all-gather of w16.  theta/m/v are then valid
                                   only on smpu_shard_ranges; per element the arithmetic is unchanged.        */
-    int32_t fuse_final;        /* world == 1 (ignored above): 1 (default) fuses the last micro-batch's accumulation
-                                  into Adam -- one pass of 30 B/element instead of K1's 6 + Adam's 28 (28 instead
-                                  of 4 + 28 at c = 1).  The overflow decision needs all of R, so the update is
-                                  computed speculatively into a second copy of theta/m/v (+12 B per parameter)
-                                  that becomes current only if R was finite; on a skip w16 is re-cast from the
-                                  current theta.  Same arithmetic per element, bitwise (tested); R itself is then
-                                  never stored (SMPU_STATE_ACCUM).  0: accumulate, decide, then Adam.            */
+    int32_t fuse_final;        /* world == 1 (ignored above).  0 (default): accumulate, decide, then Adam -- w16 changes
+                                  only inside smpu_step (SURVEY 8(b)'s contract).  1 (opt-in): fuse the last
+                                  micro-batch's accumulation into Adam -- one pass of 30 B/element instead of K1's
+                                  6 + Adam's 28 (28 instead of 4 + 28 at c = 1).  The overflow decision needs all of R,
+                                  so the update is computed speculatively into a second copy of theta/m/v (+12 B per
+                                  parameter) that becomes current only if R was finite; w16 is then rewritten by the
+                                  last micro-batch's accumulate call and re-cast on a skip.  Same arithmetic per
+                                  element, bitwise (tested); R itself is never stored (SMPU_STATE_ACCUM).          */
     int32_t accum_fp32;        /* 0 (default, the north star's fp16 accumulation, reading Z1).  1: SURVEY Z1's knob --
                                   an fp32 accumulator (+4 B per parameter): A32 = fp32(g_1), A32 = fl32(A32 + g_k),
                                   and the last micro-batch writes the rank's fp16 gradient rn16(A32) into the fp16
@@ -129,9 +130,10 @@ enum {
     SMPU_STATE_M = 1,          /* fp32[n] Adam first moment                                               */
     SMPU_STATE_V = 2,          /* fp32[n] Adam second moment                                              */
     SMPU_STATE_W16 = 3,        /* fp16[n] model weights (the re-cast copy)                                */
-    SMPU_STATE_ACCUM = 4,      /* fp16[n] gradient accumulator: after step, the reduced gradient R; with
-                                  fuse_final at world 1 the sum of the first c - 1 micro-batches instead
-                                  (untouched at c = 1), because R is consumed without being stored        */
+    SMPU_STATE_ACCUM = 4,      /* fp16[n] gradient accumulator: after step, the reduced gradient R (sharded: on
+                                  this rank's shard ranges); with fuse_final = 1 at world 1 the sum of the
+                                  first c - 1 micro-batches instead (untouched at c = 1), because R is then
+                                  consumed without being stored                                           */
     SMPU_STATE_SCALARS = 5     /* int64[4] = {e, clean_streak, num_updates, attempts}                     */
 };
 
@@ -211,11 +213,11 @@ smpu_status smpu_allreduce_impl(const smpu_ctx* ctx, int* impl);
 /* Bucket boundaries chosen at init (same as smpu_plan_buckets with cfg->bucket_bytes unless split_tensors). */
 smpu_status smpu_buckets(const smpu_ctx* ctx, int* n_buckets, int64_t* bucket_begin /* or NULL */);
 
-/* Device fp16[n] weights (library-owned, valid until smpu_destroy).  Rewritten by smpu_step, in stream order on
- * the stream passed to it -- and, with fuse_final at world 1, already by the last micro-batch's accumulate call
- * (or each bucket's, in stream order on its stream: a bucket is handed over once its gradients are done, so the
- * backward no longer reads those weights); a skipped update restores them in smpu_step.  Read them for the next
- * forward after smpu_step. */
+/* Device fp16[n] weights (library-owned, valid until smpu_destroy).  Rewritten only by smpu_step, in stream order
+ * on the stream passed to it.  Exception, opt-in: with fuse_final = 1 at world 1 they are already
+ * rewritten by the last micro-batch's accumulate call (or each bucket's, in stream order on its stream: a bucket is
+ * handed over once its gradients are done, so the backward no longer reads those weights); a skipped update
+ * restores them in smpu_step.  Read them for the next forward after smpu_step. */
 smpu_status smpu_weights_fp16(const smpu_ctx* ctx, const void** dev_w16);
 
 /* Device fp32 scalar holding the current loss scale 2^e ("we scale the loss right after the forward

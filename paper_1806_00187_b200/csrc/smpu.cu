@@ -979,7 +979,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->bucket_bytes = int64_t(150) << 20;
     c->allreduce = SMPU_AR_AUTO;
     c->sharded = 0;
-    c->fuse_final = 1;
+    c->fuse_final = 0;
     c->accum_fp32 = 0;
     c->split_tensors = 0;
     c->ar_ctas = 0;

@@ -14,8 +14,11 @@ RTOL_100 = 1e-4
 
 
 def lib_cfg(wl, ocfg: O.Config | None = None, **kw):
+    """The library config of a test workload.  fuse_final defaults to 1 HERE (the library's default is 0) so that the
+    runners keep exercising the fused last micro-batch beside the explicit fuse_final = 0 ctxs they compare with."""
     from paper_1806_00187_b200 import smpu
     ocfg = ocfg or O.Config()
+    kw.setdefault("fuse_final", 1)
     c = smpu.config_default(peak_lr=ocfg.peak_lr, warmup_updates=ocfg.warmup, beta1=ocfg.beta1, beta2=ocfg.beta2,
                             eps=ocfg.eps, init_scale_log2=ocfg.init_scale_log2, min_scale_log2=ocfg.min_scale_log2,
                             max_scale_log2=ocfg.max_scale_log2, growth_interval=ocfg.growth,

@@ -40,7 +40,8 @@ def test_every_declared_symbol_is_exported(P):
 def test_abi_version_and_defaults(P):
     assert P.abi_version() == 3
     c = P.config_default()
-    assert (c.allreduce, c.sharded, c.fuse_final, c.accum_fp32, c.split_tensors) == (0, 0, 1, 0, 0)
+    # fuse_final is opt-in: the default ctx keeps SURVEY 8(b)'s contract (w16 changes only inside smpu_step)
+    assert (c.allreduce, c.sharded, c.fuse_final, c.accum_fp32, c.split_tensors) == (0, 0, 0, 0, 0)
     assert (c.peak_lr, c.warmup_updates, c.beta1, c.beta2, c.eps) == (5e-4, 4000, 0.9, 0.98, 1e-8)
     assert (c.init_scale_log2, c.min_scale_log2, c.max_scale_log2, c.growth_interval) == (7, -5, 24, 2000)
     assert c.bucket_bytes == 150 << 20                                                                # P:212 fn
