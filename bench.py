@@ -46,6 +46,10 @@ def parse():
                          "all-gather of w16 (bitwise equal to the replicated update); auto = replicated headline "
                          "with the sharded variant timed beside it when the fused all-reduce is available")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
+    ap.add_argument("--ar-tail-split", type=int, default=None,
+                    help="smpu_config.ar_tail_split (replicated, W > 1): the last bucket's all-reduce in pieces, "
+                         "each followed by its Adam; default: the library's")
+    ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
     ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
                     help="input family (SURVEY 8(d.2)); real_sparse = G_real with the row-sparse embedding gradient "
                          "(Zipf(1.1) token rows); the performance-independence check times all four")
@@ -723,7 +727,10 @@ def main_ours(args):
 
     def make_cfg(sharded, fuse_final=args.fuse_final):
         cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)), allreduce=ar,
-                               sharded=int(sharded), fuse_final=fuse_final, accum_fp32=int(args.accum_fp32))
+                               sharded=int(sharded), fuse_final=fuse_final, accum_fp32=int(args.accum_fp32),
+                               ar_ctas=args.ar_ctas)
+        if args.ar_tail_split is not None:
+            cfg.ar_tail_split = args.ar_tail_split
         # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
         cfg.growth_interval = 1 << 40
         return cfg

@@ -103,7 +103,11 @@ struct smpu_ctx {
     size_t w16_off = 0;                                     // w16 inside the symmetric window
     std::vector<std::vector<std::pair<int64_t, int64_t>>> shard;   // per bucket: this rank's element ranges
     cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
-    std::vector<cudaEvent_t> ready, ar_done;
+    std::vector<cudaEvent_t> ready;
+    // all-reduce launches of bucket b: pieces[b] = element boundaries (one piece unless smpu_config.ar_tail_split
+    // pipelines the last bucket), ar_done[b][i] = piece i reduced
+    std::vector<std::vector<int64_t>> pieces;
+    std::vector<std::vector<cudaEvent_t>> ar_done;
     cudaEvent_t comm_done = nullptr, order_ev = nullptr, dec_ev = nullptr, k2_done = nullptr;
     cudaStream_t last_stream = nullptr;
     bool have_order = false;
@@ -590,17 +594,20 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
         int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
         cudaStream_t cs = ctx->comm_stream;
         CK(cudaStreamWaitEvent(cs, ctx->ready[b], 0));
-        {
-            Timed t(ctx, SMPU_ALLREDUCE, cs);
-            if (ctx->ar_impl == SMPU_AR_FUSED) {
-                smpu_status st = launch_ar_fused(ctx, lo, hi, cs);
-                if (st != SMPU_OK) return st;
-            } else {
-                NK(ncclAllReduce(ctx->acc + lo, ctx->acc + lo, (size_t)(hi - lo), ncclFloat16, ncclSum, ctx->comm,
-                                 cs));
+        const auto& pc = ctx->pieces[b];
+        for (size_t i = 0; i + 1 < pc.size(); ++i) {
+            {
+                Timed t(ctx, SMPU_ALLREDUCE, cs);
+                if (ctx->ar_impl == SMPU_AR_FUSED) {
+                    smpu_status st = launch_ar_fused(ctx, pc[i], pc[i + 1], cs);
+                    if (st != SMPU_OK) return st;
+                } else {
+                    NK(ncclAllReduce(ctx->acc + pc[i], ctx->acc + pc[i], (size_t)(pc[i + 1] - pc[i]), ncclFloat16,
+                                     ncclSum, ctx->comm, cs));
+                }
             }
+            CK(cudaEventRecord(ctx->ar_done[b][i], cs));
         }
-        CK(cudaEventRecord(ctx->ar_done[b], cs));
         ctx->next_issue++;
     }
     if (ctx->next_issue == ctx->nb) CK(cudaEventRecord(ctx->comm_done, ctx->comm_stream));
@@ -615,12 +622,15 @@ smpu_status group_issue_buckets(smpu_ctx* ctx) {
     while (g->next_issue < ctx->nb && g->arrived[g->next_issue] == g->world) {
         const int b = g->next_issue;
         for (smpu_ctx* q : g->m) CK(cudaStreamWaitEvent(g->comm, q->ready[b], 0));
-        smpu_status st = launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world, ctx->bbegin[b],
-                                        ctx->bbegin[b + 1], g->comm);
-        if (st != SMPU_OK) return st;
-        for (smpu_ctx* q : g->m) {
-            q->launches[SMPU_ALLREDUCE]++;
-            CK(cudaEventRecord(q->ar_done[b], g->comm));
+        const auto& pc = ctx->pieces[b];
+        for (size_t i = 0; i + 1 < pc.size(); ++i) {
+            smpu_status st = launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world, pc[i],
+                                            pc[i + 1], g->comm);
+            if (st != SMPU_OK) return st;
+            for (smpu_ctx* q : g->m) {
+                q->launches[SMPU_ALLREDUCE]++;
+                CK(cudaEventRecord(q->ar_done[b][i], g->comm));
+            }
         }
         g->arrived[b] = 0;
         g->next_issue++;
@@ -679,11 +689,14 @@ smpu_status enqueue_adam(smpu_ctx* ctx) {
     cudaStream_t ks = ctx->k2_stream;
     CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
     for (int b = 0; b < ctx->nb; ++b) {
-        int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
-        CK(cudaStreamWaitEvent(ks, ctx->ar_done[b], 0));
-        Timed t(ctx, SMPU_K2, ks);
-        smpu_status st = ctx->sharded ? launch_k2_shard(ctx, b, DEC_APPLY, ks) : launch_k2(ctx, lo, hi, DEC_APPLY, ks);
-        if (st != SMPU_OK) return st;
+        const auto& pc = ctx->pieces[b];
+        for (size_t i = 0; i + 1 < pc.size(); ++i) {   // each piece right behind its all-reduce
+            CK(cudaStreamWaitEvent(ks, ctx->ar_done[b][i], 0));
+            Timed t(ctx, SMPU_K2, ks);
+            smpu_status st = ctx->sharded ? launch_k2_shard(ctx, b, DEC_APPLY, ks)
+                                          : launch_k2(ctx, pc[i], pc[i + 1], DEC_APPLY, ks);
+            if (st != SMPU_OK) return st;
+        }
     }
     CK(cudaEventRecord(ctx->k2_done, ks));
     return SMPU_OK;
@@ -889,9 +902,10 @@ smpu_status check_cfg(const smpu_config* c) {
     if (c->bucket_bytes < 2) return set_err(SMPU_EINVAL, "bucket_bytes must be >= 2");
     if (c->ar_ctas < 0 || (c->ar_threads != 256 && c->ar_threads != 512) ||
         (c->ar_vec_bytes != 16 && c->ar_vec_bytes != 32) || (c->ar_unroll != 1 && c->ar_unroll != 2) ||
-        (c->ar_mcast != 0 && c->ar_mcast != 1) || (c->pdl != 0 && c->pdl != 1))
+        (c->ar_mcast != 0 && c->ar_mcast != 1) || (c->pdl != 0 && c->pdl != 1) || c->ar_tail_split < 1 ||
+        c->ar_tail_split > 64)
         return set_err(SMPU_EINVAL, "bad all-reduce shape: ar_ctas >= 0, ar_threads 256|512, ar_vec_bytes 16|32, "
-                                    "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1");
+                                    "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1, ar_tail_split 1..64");
     if (c->ar_mcast && c->ar_vec_bytes != 32)
         return set_err(SMPU_EINVAL, "ar_mcast needs ar_vec_bytes = 32");
     return SMPU_OK;
@@ -926,7 +940,8 @@ void free_ctx(smpu_ctx* c) {
     if (c->ring_host) cudaFreeHost(c->ring_host);
     for (auto& e : c->ring_ev) if (e) cudaEventDestroy(e);
     for (auto& e : c->ready) if (e) cudaEventDestroy(e);
-    for (auto& e : c->ar_done) if (e) cudaEventDestroy(e);
+    for (auto& v : c->ar_done)
+        for (auto& e : v) if (e) cudaEventDestroy(e);
     if (c->dec_ev) cudaEventDestroy(c->dec_ev);
     if (c->k2_done) cudaEventDestroy(c->k2_done);
     if (c->tail_ev) cudaEventDestroy(c->tail_ev);
@@ -988,6 +1003,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->ar_unroll = 1;
     c->ar_mcast = 0;
     c->pdl = 1;
+    c->ar_tail_split = 1;
     return SMPU_OK;
 }
 
@@ -1170,8 +1186,25 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
     for (auto& e : ctx->ring_ev) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->ready.resize(ctx->nb);
     for (auto& e : ctx->ready) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // all-reduce pieces: one per bucket; with ar_tail_split (replicated layout) the last bucket is cut into that
+    // many pieces on 256-element boundaries, each all-reduced and then updated on its own, so that Adam of piece i
+    // overlaps the all-reduce of piece i + 1 in the update's exposed tail.  Values never change (elementwise).
+    ctx->pieces.resize(ctx->nb);
     ctx->ar_done.resize(ctx->nb);
-    for (auto& e : ctx->ar_done) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int b = 0; b < ctx->nb; ++b) {
+        const int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
+        const int split = (b == ctx->nb - 1 && !cfg->sharded && world > 1) ? cfg->ar_tail_split : 1;
+        auto& pc = ctx->pieces[b];
+        pc.push_back(lo);
+        const int64_t step = (hi - lo + split - 1) / split;
+        for (int i = 1; i < split; ++i) {
+            const int64_t cut = (lo + i * step + 255) & ~(int64_t)255;
+            if (cut > pc.back() && cut < hi) pc.push_back(cut);
+        }
+        pc.push_back(hi);
+        ctx->ar_done[b].assign(pc.size() - 1, nullptr);
+        for (auto& e : ctx->ar_done[b]) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     IK(cudaEventCreateWithFlags(&ctx->dec_ev, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->k2_done, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->tail_ev, cudaEventDisableTiming));
@@ -1252,10 +1285,12 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         // window registration or in LSA barriers the others never join.  EINVAL on every rank instead.
         static const char* kField[] = {"update_freq", "bucket_bytes", "split_tensors", "sharded", "accum_fp32",
                                        "allreduce", "ar_ctas", "ar_threads", "ar_vec_bytes", "ar_unroll", "ar_mcast",
-                                       "n (parameter count)", "n_buckets", "symmetric-memory allocation"};
+                                       "ar_tail_split", "n (parameter count)", "n_buckets",
+                                       "symmetric-memory allocation"};
         const int64_t mine[] = {cfg->update_freq, cfg->bucket_bytes, cfg->split_tensors, cfg->sharded,
                                 cfg->accum_fp32, cfg->allreduce, ctx->grid_ar, cfg->ar_threads, cfg->ar_vec_bytes,
-                                cfg->ar_unroll, cfg->ar_mcast, n, ctx->nb, ctx->acc_from_nccl ? 1 : 0};
+                                cfg->ar_unroll, cfg->ar_mcast, cfg->ar_tail_split, n, ctx->nb,
+                                ctx->acc_from_nccl ? 1 : 0};
         constexpr int K = sizeof(mine) / sizeof(mine[0]);
         int64_t mn[K], mx[K];
         IN(agree(ctx->comm, s0, mine, K, mn, mx), "rank agreement all-reduce");

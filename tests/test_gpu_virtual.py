@@ -70,12 +70,13 @@ def _feed(members, grads, toks, mode, rng, bb):
         raise ValueError(mode)
 
 
-def _run(world, family="real", sharded=False, mode="calls", updates=6):
+def _run(world, family="real", sharded=False, mode="calls", updates=6, **cfg_kw):
     import paper_1806_00187_b200 as P
     wl = _workload(world, family, updates)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
-    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, bucket_bytes=400_000, sharded=int(sharded)), world=world)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, bucket_bytes=400_000, sharded=int(sharded), **cfg_kw),
+                         world=world)
     members = grp.members
     bb = members[0].bucket_begin
     assert len(bb) - 1 >= 2 and any(int(x) % 16 for x in bb[1:-1]), "buckets must cut off the vector grid"
@@ -148,6 +149,13 @@ def test_virtual_buckets_out_of_order(world, sharded):
     """Bucket-wise last micro-batches, buckets and ranks interleaved at random: all-reduces still issue in canonical
     bucket order and R is unchanged."""
     _run(world, "real", sharded, mode="buckets")
+
+
+@pytest.mark.parametrize("world,split", [(4, 5), (2, 3)])
+def test_virtual_tail_split(world, split):
+    """smpu_config.ar_tail_split: the last bucket all-reduced as `split` pieces, Adam of each right behind it; same
+    bits as one launch (the oracle's)."""
+    _run(world, "real", False, mode="buckets", ar_tail_split=split)
 
 
 @pytest.mark.parametrize("world,sharded", [(4, False), (7, True)])
