@@ -206,10 +206,12 @@ def micro_grad_sample(wl: Workload, lay: Layout, idx: np.ndarray, u: int, r: int
         if sel.any():
             mask = embed_mask(wl, rows, u, r, k)
             out[sel] = np.where(mask[(idx[sel] - a) // wl.embed_row].astype(bool), out[sel], 0)
-    pos = {int(v): j for j, v in enumerate(idx)}
-    for i, bits in overrides(wl, u, r, k):
-        if i in pos:
-            out[pos[i]] = bits
+    ov = overrides(wl, u, r, k)
+    if ov:
+        pos = {int(v): j for j, v in enumerate(idx)}
+        for i, bits in ov:
+            if i in pos:
+                out[pos[i]] = bits
     return out
 
 
