@@ -73,6 +73,8 @@ def parse():
                          "library, buckets handed over as backward finishes them (SURVEY f3; Table 1-style tok/s)")
     ap.add_argument("--tokens", type=int, default=3500, help="train: token budget per micro-batch (P:317)")
     ap.add_argument("--sent-len", type=int, default=28, help="train: sentence length of the synthetic batches")
+    ap.add_argument("--eager-producer", action="store_true",
+                    help="train: run the producer eagerly (Python-launch bound) instead of as a CUDA graph per shape")
     ap.add_argument("--no-overlap", action="store_true",
                     help="train: hand the last micro-batch over after backward (no overlap) instead of per bucket")
     ap.add_argument("--e2e-steps", type=int, default=4)
@@ -283,7 +285,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
                              "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def synth_ntokens(wl, u, r, k):
@@ -466,8 +468,9 @@ def run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, thet
     through a world = 1 ctx."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "producer"))
-    from transformer import Producer, TransformerBig, device_view
+    from transformer import GraphedProducer, Producer, TransformerBig, device_view
     c, n = wl.update_freq, lay.n
+    side = torch.cuda.Stream(device=f"cuda:{local}")
     dropout = 0.1 if "enfr" in wl.name else 0.3                       # P:101
 
     def setup(st, seed):
@@ -485,8 +488,29 @@ def run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, thet
         per = np.bincount(tb, minlength=len(bb) - 1)
         return tb, per, bb
 
-    def one(st, prod, grad, batches, overlap):
+    def one(st, prod, grad, batches, overlap, gp=None):
         g16 = grad.view(torch.int16)
+        if gp is not None:
+            # graphed producer: the backward records each bucket's completion as an event inside its graph; the
+            # library takes bucket b on a second stream as soon as that event fires
+            for k in range(c - 1):
+                src, ti, to, nt = batches[k]
+                gp.micro(src, ti, to)
+                st.accumulate(g16, nt, stream)
+            src, ti, to, nt = batches[c - 1]
+            events, _ = gp.micro(src, ti, to)
+            if not overlap:
+                st.accumulate(g16, nt, stream)
+                st.step(stream, wait=False)
+                return
+            tb, per, bb = bucket_of(st)
+            st.micro_begin(nt)
+            for b in range(len(bb) - 1):
+                side.wait_event(events[b])
+                st.accumulate_bucket(b, g16[int(bb[b]):int(bb[b + 1])], side)
+            st.step(side, wait=False)
+            stream.wait_stream(side)          # the next replay rewrites the gradient buffer and reads w16
+            return
         for k in range(c - 1):
             src, ti, to, nt = batches[k]
             prod.micro(src, ti, to)
@@ -510,15 +534,19 @@ def run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, thet
 
     def timed(st, w, overlap, seed):
         prod, grad, batches = setup(st, seed)
+        gp = None
+        if not args.eager_producer:
+            tb, per, bb = bucket_of(st)
+            gp = GraphedProducer(prod, tb, len(bb) - 1)
         for _ in range(max(1, args.warmup)):
-            one(st, prod, grad, batches, overlap)
+            one(st, prod, grad, batches, overlap, gp)
         torch.cuda.synchronize()
         _barrier(w)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with Clocks(local) as clk:
             a.record(stream)
             for _ in range(args.steps):
-                one(st, prod, grad, batches, overlap)
+                one(st, prod, grad, batches, overlap, gp)
             b.record(stream)
             torch.cuda.synchronize()
         _barrier(w)
@@ -548,6 +576,7 @@ def run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, thet
            "model_flops_per_token": fpt, "model_tflops_per_s_per_gpu": fpt * tok / world / (ms * 1e-3) / 1e12,
            "last_result": {k: last[k] for k in ("applied", "overflow", "scale_log2_used", "lr", "num_updates")},
            "overlap": "per-bucket handover from backward hooks (P:211-212)" if overlap else "after backward",
+           "producer_mode": "eager" if args.eager_producer else "CUDA graph per batch shape (bucket events in-graph)",
            "config": {"workload": wl.name, "update_freq": c, "world": world, "bucket_mib": args.bucket_mib,
                       "tokens_per_micro_budget": args.tokens, "sent_len": args.sent_len, "dropout": dropout,
                       "label_smoothing": 0.1, "data": "synthetic uniform token ids (no dataset)",
@@ -750,7 +779,7 @@ def main_ours(args):
             del grads
             out = run_train(args, P, wl, lay, step, stream, world, rank, local, make_cfg, theta0)
         if out is not None:
-            print(json.dumps(out), flush=True)
+            emit(out)
         if world > 1:
             dist.destroy_process_group()
         return
@@ -930,7 +959,7 @@ def main_ours(args):
         O.set_threads(cores)
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                                "value_1_thread": v1, "sample_1_thread": sample1, "cpu_model": cpu_model()}
-    print(json.dumps(out), flush=True)
+    emit(out)
     if world > 1:
         dist.destroy_process_group()
 
@@ -939,6 +968,25 @@ def ctypes_sizeof_result():
     import ctypes
     from paper_1806_00187_b200 import smpu
     return ctypes.sizeof(smpu.StepResult)
+
+
+_JSON_OUT = None
+
+
+def keep_stdout_for_json():
+    """From here on, anything written to file descriptor 1 -- NCCL's C-level `NCCL version ...` banner included --
+    goes to stderr; the one JSON line goes to the original stdout (emit), so the driver reads exactly one line."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
 
 
 def _max_over_ranks(x, world):
@@ -994,8 +1042,9 @@ def load_traffic(kernel, workload_name):
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        spawn_ranks(args)
+        spawn_ranks(args)        # the ranks inherit the real stdout; rank 0 prints the line
         return
+    keep_stdout_for_json()
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -179,3 +179,61 @@ class Producer:
         w = sum(nm_n for nm, nm_n in zip(m.names, m.numel) if nm.endswith(".weight") and "ln" not in nm
                 and nm != "embed_tokens.weight")
         return 6 * (w + m.vocab * m.d)
+
+
+class GraphedProducer:
+    """Producer.micro captured once per batch shape as a CUDA graph -- forward, backward and the per-tensor gradient
+    copies into the packed buffer -- and replayed, so the producer runs at GPU speed instead of Python / launch
+    speed (CUDA graphs instead of a tracing compiler).  Inside the graph, the completion of bucket b's last tensor
+    gradient records the external event `bucket_done[b]`: a consumer stream can wait on it and hand bucket b to
+    the library while the rest of the backward still runs."""
+
+    def __init__(self, prod: Producer, tensor_bucket, n_buckets):
+        self.p = prod
+        self.tb = list(tensor_bucket)
+        self.nb = n_buckets
+        self.graphs = {}
+
+    def _capture(self, shape):
+        m, p = self.p.m, self.p
+        S, Ls, Lt = shape
+        dev = m.device
+        st = {"src": torch.randint(4, m.vocab, (S, Ls), device=dev, generator=p.gen),
+              "ti": torch.randint(4, m.vocab, (S, Lt), device=dev, generator=p.gen),
+              "to": torch.randint(4, m.vocab, (S, Lt), device=dev, generator=p.gen)}
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):               # warm-up outside the graph (allocator, kernel selection)
+            for _ in range(3):
+                p.micro(st["src"], st["ti"], st["to"])
+        torch.cuda.current_stream(dev).wait_stream(side)
+        events = [torch.cuda.Event(external=True) for _ in range(self.nb)]
+        left = np.bincount(self.tb, minlength=self.nb)
+
+        def on_tensor(j):
+            b = self.tb[j]
+            left[b] -= 1
+            if left[b] == 0:
+                events[b].record()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            loss = p.micro(st["src"], st["ti"], st["to"], on_tensor=on_tensor)
+        assert (left == 0).all(), "every bucket must complete inside the graph"
+        self.graphs[shape] = (g, st, events, loss)
+        return self.graphs[shape]
+
+    def forget(self):
+        """Drop every captured graph (and its private memory pool)."""
+        self.graphs.clear()
+        torch.cuda.empty_cache()
+
+    def micro(self, src, tgt_in, tgt_out):
+        """Replay the graph of this batch shape on the current stream; returns the bucket events (recorded by the
+        replay) and the static loss tensor."""
+        shape = (src.shape[0], src.shape[1], tgt_in.shape[1])
+        g, st, events, loss = self.graphs.get(shape) or self._capture(shape)
+        st["src"].copy_(src)
+        st["ti"].copy_(tgt_in)
+        st["to"].copy_(tgt_out)
+        g.replay()
+        return events, loss

@@ -40,9 +40,10 @@ def main():
     ap.add_argument("--measure", type=int, default=240)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_straggler_measured.txt"))
     ap.add_argument("--corpus", type=int, default=4_500_000)
+    ap.add_argument("--eager", action="store_true", help="time the eager producer (launch-bound) instead of graphs")
     args = ap.parse_args()
     import torch
-    from transformer import Producer, TransformerBig
+    from transformer import GraphedProducer, Producer, TransformerBig
 
     rng = np.random.default_rng(0)
     n = args.corpus
@@ -56,6 +57,7 @@ def main():
     model = TransformerBig(wl.tensors, w16, dropout=0.3, max_len=256)
     grad = torch.empty(nparam, dtype=torch.float16, device="cuda")
     prod = Producer(model, grad, torch.tensor([128.0], device="cuda"), seed=0)
+    gp = None if args.eager else GraphedProducer(prod, [0] * len(wl.tensors), 1)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1)
 
@@ -66,15 +68,18 @@ def main():
     def time_shape(s, ls, lt, reps=3):
         a = torch.randint(4, model.vocab, (s, ls), device="cuda", generator=gen)
         t = torch.randint(4, model.vocab, (s, lt + 1), device="cuda", generator=gen)
-        prod.micro(a, t[:, :-1], t[:, 1:])          # warm-up (allocator, kernel selection for this shape)
+        run = prod.micro if gp is None else gp.micro
+        run(a, t[:, :-1], t[:, 1:])                 # warm-up (allocator, kernel selection / graph capture)
         out = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            prod.micro(a, t[:, :-1], t[:, 1:])
+            run(a, t[:, :-1], t[:, 1:])
             e1.record()
             torch.cuda.synchronize()
             out.append(e0.elapsed_time(e1) * 1e-3)
+        if gp is not None:
+            gp.forget()                             # one graph (and its activation pool) per shape at a time
         return float(np.median(out))
 
     def measure(order, begin, k):
@@ -94,7 +99,8 @@ def main():
     shp2, t2 = measure(o2, b2, args.measure)
 
     lines = [__doc__.strip().split("\n\n")[0], "",
-             f"GPU: {torch.cuda.get_device_name()}; model Transformer-big En-De ({nparam} params), fp16 fwd+bwd",
+             f"GPU: {torch.cuda.get_device_name()}; model Transformer-big En-De ({nparam} params), fp16 fwd+bwd, "
+             f"{'eager PyTorch (launch-bound)' if gp is None else 'one CUDA graph per sub-batch shape'}",
              f"token-budget 3.5k: {len(b1) - 1} sub-batches (paper: 44K, P:319); measured {len(t1)}: "
              f"mean {t1.mean()*1e3:.2f} ms, min/mean {t1.min()/t1.mean():.2f}, max/mean {t1.max()/t1.mean():.2f} "
              f"(paper Fig. 6 on V100: 0.45 / 2.07), CV {t1.std()/t1.mean():.3f}",
