@@ -46,8 +46,8 @@ def parse():
                          "all-gather of w16 (bitwise equal to the replicated update); auto = replicated headline "
                          "with the sharded variant timed beside it when the fused all-reduce is available")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
-    ap.add_argument("--ar-tail-split", type=int, default=None,
-                    help="smpu_config.ar_tail_split (replicated, W > 1): the last bucket's all-reduce in pieces, "
+    ap.add_argument("--ar-pieces", type=int, default=None,
+                    help="smpu_config.ar_pieces (replicated, W > 1): the last bucket's all-reduce in pieces, "
                          "each followed by its Adam; default: the library's")
     ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
     ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
@@ -758,8 +758,8 @@ def main_ours(args):
         cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)), allreduce=ar,
                                sharded=int(sharded), fuse_final=fuse_final, accum_fp32=int(args.accum_fp32),
                                ar_ctas=args.ar_ctas)
-        if args.ar_tail_split is not None:
-            cfg.ar_tail_split = args.ar_tail_split
+        if args.ar_pieces is not None:
+            cfg.ar_pieces = args.ar_pieces
         # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
         cfg.growth_interval = 1 << 40
         return cfg

@@ -101,10 +101,11 @@ typedef struct {
                                   rank has no NVLS); 0 (default): unicast peer stores                                 */
     int32_t pdl;               /* world == 1: programmatic dependent launch of the K1 -> K0 -> K2 chain, 1 (default)
                                   or 0.  Per rank; no effect at world > 1.                                           */
-    int32_t ar_tail_split;     /* world > 1, replicated layout: all-reduce the LAST bucket (ready last, so its
-                                  all-reduce and Adam are the update's exposed tail) as this many consecutive pieces,
-                                  Adam of each piece right behind its all-reduce, so the two pipeline.  1 (default) =
-                                  one launch; 1..64.  Collective: compared across ranks like the ar_* fields.       */
+    int32_t ar_pieces;         /* world > 1, replicated layout: all-reduce every bucket as this many consecutive
+                                  pieces, Adam of each piece right behind its all-reduce, so that the Adam chain
+                                  starts after the first piece rather than the first whole bucket and the two
+                                  pipeline.  1 (default) = one launch per bucket; 1..64.  Collective: compared across
+                                  ranks like the ar_* fields.                                                        */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */

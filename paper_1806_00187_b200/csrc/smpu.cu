@@ -104,8 +104,8 @@ struct smpu_ctx {
     std::vector<std::vector<std::pair<int64_t, int64_t>>> shard;   // per bucket: this rank's element ranges
     cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
     std::vector<cudaEvent_t> ready;
-    // all-reduce launches of bucket b: pieces[b] = element boundaries (one piece unless smpu_config.ar_tail_split
-    // pipelines the last bucket), ar_done[b][i] = piece i reduced
+    // all-reduce launches of bucket b: pieces[b] = element boundaries (one piece unless smpu_config.ar_pieces
+    // pipelines them), ar_done[b][i] = piece i reduced
     std::vector<std::vector<int64_t>> pieces;
     std::vector<std::vector<cudaEvent_t>> ar_done;
     cudaEvent_t comm_done = nullptr, order_ev = nullptr, dec_ev = nullptr, k2_done = nullptr;
@@ -902,10 +902,10 @@ smpu_status check_cfg(const smpu_config* c) {
     if (c->bucket_bytes < 2) return set_err(SMPU_EINVAL, "bucket_bytes must be >= 2");
     if (c->ar_ctas < 0 || (c->ar_threads != 256 && c->ar_threads != 512) ||
         (c->ar_vec_bytes != 16 && c->ar_vec_bytes != 32) || (c->ar_unroll != 1 && c->ar_unroll != 2) ||
-        (c->ar_mcast != 0 && c->ar_mcast != 1) || (c->pdl != 0 && c->pdl != 1) || c->ar_tail_split < 1 ||
-        c->ar_tail_split > 64)
+        (c->ar_mcast != 0 && c->ar_mcast != 1) || (c->pdl != 0 && c->pdl != 1) || c->ar_pieces < 1 ||
+        c->ar_pieces > 64)
         return set_err(SMPU_EINVAL, "bad all-reduce shape: ar_ctas >= 0, ar_threads 256|512, ar_vec_bytes 16|32, "
-                                    "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1, ar_tail_split 1..64");
+                                    "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1, ar_pieces 1..64");
     if (c->ar_mcast && c->ar_vec_bytes != 32)
         return set_err(SMPU_EINVAL, "ar_mcast needs ar_vec_bytes = 32");
     return SMPU_OK;
@@ -1003,7 +1003,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->ar_unroll = 1;
     c->ar_mcast = 0;
     c->pdl = 1;
-    c->ar_tail_split = 1;
+    c->ar_pieces = 1;
     return SMPU_OK;
 }
 
@@ -1186,14 +1186,15 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
     for (auto& e : ctx->ring_ev) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->ready.resize(ctx->nb);
     for (auto& e : ctx->ready) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    // all-reduce pieces: one per bucket; with ar_tail_split (replicated layout) the last bucket is cut into that
-    // many pieces on 256-element boundaries, each all-reduced and then updated on its own, so that Adam of piece i
-    // overlaps the all-reduce of piece i + 1 in the update's exposed tail.  Values never change (elementwise).
+    // all-reduce pieces: with ar_pieces = P (replicated layout, world > 1) every bucket is cut into P pieces on
+    // 256-element boundaries, each all-reduced and then updated on its own, so that Adam of piece i overlaps the
+    // all-reduce of piece i + 1 and the Adam chain starts after the first piece instead of the first bucket.  Values
+    // never change (elementwise).
     ctx->pieces.resize(ctx->nb);
     ctx->ar_done.resize(ctx->nb);
     for (int b = 0; b < ctx->nb; ++b) {
         const int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
-        const int split = (b == ctx->nb - 1 && !cfg->sharded && world > 1) ? cfg->ar_tail_split : 1;
+        const int split = (!cfg->sharded && world > 1) ? cfg->ar_pieces : 1;
         auto& pc = ctx->pieces[b];
         pc.push_back(lo);
         const int64_t step = (hi - lo + split - 1) / split;
@@ -1285,11 +1286,11 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         // window registration or in LSA barriers the others never join.  EINVAL on every rank instead.
         static const char* kField[] = {"update_freq", "bucket_bytes", "split_tensors", "sharded", "accum_fp32",
                                        "allreduce", "ar_ctas", "ar_threads", "ar_vec_bytes", "ar_unroll", "ar_mcast",
-                                       "ar_tail_split", "n (parameter count)", "n_buckets",
+                                       "ar_pieces", "n (parameter count)", "n_buckets",
                                        "symmetric-memory allocation"};
         const int64_t mine[] = {cfg->update_freq, cfg->bucket_bytes, cfg->split_tensors, cfg->sharded,
                                 cfg->accum_fp32, cfg->allreduce, ctx->grid_ar, cfg->ar_threads, cfg->ar_vec_bytes,
-                                cfg->ar_unroll, cfg->ar_mcast, cfg->ar_tail_split, n, ctx->nb,
+                                cfg->ar_unroll, cfg->ar_mcast, cfg->ar_pieces, n, ctx->nb,
                                 ctx->acc_from_nccl ? 1 : 0};
         constexpr int K = sizeof(mine) / sizeof(mine[0]);
         int64_t mn[K], mx[K];

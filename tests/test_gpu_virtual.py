@@ -152,10 +152,10 @@ def test_virtual_buckets_out_of_order(world, sharded):
 
 
 @pytest.mark.parametrize("world,split", [(4, 5), (2, 3)])
-def test_virtual_tail_split(world, split):
-    """smpu_config.ar_tail_split: the last bucket all-reduced as `split` pieces, Adam of each right behind it; same
-    bits as one launch (the oracle's)."""
-    _run(world, "real", False, mode="buckets", ar_tail_split=split)
+def test_virtual_pieces(world, split):
+    """smpu_config.ar_pieces: every bucket all-reduced as `split` pieces, Adam of each right behind it; same bits
+    as one launch per bucket (the oracle's)."""
+    _run(world, "real", False, mode="buckets", ar_pieces=split)
 
 
 @pytest.mark.parametrize("world,sharded", [(4, False), (7, True)])
