@@ -713,6 +713,24 @@ def bus_gbs(stats, steps, n, world, sharded):
             "frac_of_770_measured_peer": bus / 770.0, "in_situ": "concurrent with K1 / Adam"}
 
 
+def bind_to_gpu_numa(local):
+    """Run this rank on the CPUs NVML lists as local to its GPU, so that its pinned host buffers (the e2e inputs,
+    first-touch allocated by cudaHostAlloc) sit on the GPU's NUMA node.  Returns the CPU count, or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        cpus &= set(range(os.cpu_count() or 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        return None
+    return None
+
+
 def main_ours(args):
     import torch
     import torch.distributed as dist
@@ -722,6 +740,7 @@ def main_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    numa_cpus = bind_to_gpu_numa(local) if world > 1 else None
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -808,7 +827,8 @@ def main_ours(args):
         e2e_s = _max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, world)
         e2e = {"value": world * c * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": c * n * 2,
                "d2h_bytes_per_step": ctypes_sizeof_result(), "ms_per_step": 1000 * e2e_s,
-               "source": "pinned host fp16 micro-gradients, staged H2D inside smpu_accumulate"}
+               "source": "pinned host fp16 micro-gradients, staged H2D inside smpu_accumulate",
+               "rank_cpus_numa_local": numa_cpus}
         del host
     step.close()
     del step
