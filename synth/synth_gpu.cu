@@ -50,11 +50,11 @@ __global__ void fill_kernel(uint16_t* __restrict__ out, int64_t begin, int64_t e
     }
 }
 
-// h mod m for a small modulus m (< 2^31) with 32-bit operations only: the same value as the CPU's 64-bit `h % m`
-// (h = hi 2^32 + lo, so h mod m = ((hi mod m) (2^32 mod m) + lo mod m) mod m, every product < 2^62)
+// h mod m for a modulus m < 2^16 with 32-bit operations only: the same value as the CPU's 64-bit `h % m`
+// (h = hi 2^32 + lo, so h mod m = ((hi mod m) (2^32 mod m) + lo mod m) mod m; the product is < m^2 < 2^32)
 __device__ __forceinline__ uint32_t mod_small(uint64_t h, uint32_t m, uint32_t two32_mod_m) {
     const uint32_t hi = (uint32_t)(h >> 32) % m, lo = (uint32_t)h % m;
-    return (uint32_t)(((uint64_t)hi * two32_mod_m + lo) % m);
+    return ((hi * two32_mod_m) % m + lo) % m;
 }
 
 // 2^s exactly, for the normal range -126 <= s <= 127 (built from its exponent bits)
@@ -143,6 +143,7 @@ int synth_gpu_fill(uint16_t* dev_out, int n_tensors, const int64_t* tensor_begin
 // Same values as synth_gpu_fill in one launch; tensor_begin (nt+1) / cls (nt) are DEVICE arrays.
 int synth_gpu_fill_all(uint16_t* dev_out, int64_t n, const int64_t* dev_begin, const int32_t* dev_cls, int n_tensors,
                        int family, uint64_t key, int e, int K, void* stream) {
+    if (family == 1 && (K < 0 || 2 * (int64_t)K + 1 >= 65536)) return -2;   // mod_small's range
     size_t shmem = (size_t)(n_tensors + 1) * 8 + (size_t)n_tensors * 4;
     if (shmem > 48 * 1024) return -1;
     int64_t blocks = (n + 8 * 256 - 1) / (8 * 256);

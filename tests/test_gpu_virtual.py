@@ -264,16 +264,16 @@ def test_c3_enfr_5200_updates_virtual_w8(gold):
     mags = Magnitudes(orc.theta.copy())
     checks = {int(r[0]): tuple(map(int, r[1:])) for r in gold("scaler_trace_c3.txt")}
     inj_u = {inj["u"] for inj in wl.injections}
-    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(2)]
+    # each rank's 16 micro-batches resident, accumulated in one pass (smpu_accumulate_many: the same sums in the same
+    # order as 16 calls, bitwise -- tests/test_gpu_parity.py); the buffers are reused rank after rank, stream-ordered
+    bufs = [torch.empty(lay.n, dtype=torch.int16, device="cuda") for _ in range(c)]
     pending = []
     e = 7
     for u in range(1, wl.updates + 1):
-        j = 0
-        for k in range(1, c + 1):
-            for r in range(W):
-                synth.micro_grad_gpu(bufs[j & 1], wl, lay, u, r, k, e)
-                ms[r].accumulate(bufs[j & 1], synth.ntokens(wl, u, r, k))
-                j += 1
+        for r in range(W):
+            for k in range(1, c + 1):
+                synth.micro_grad_gpu(bufs[k - 1], wl, lay, u, r, k, e)
+            ms[r].accumulate_many(bufs, [synth.ntokens(wl, u, r, k) for k in range(1, c + 1)])
         for m in ms:
             m.step(wait=False)
         grads = [[synth.micro_grad_sample(wl, lay, idx, u, r, k, e) for k in range(1, c + 1)] for r in range(W)]
