@@ -544,6 +544,52 @@ def test_graph_direct_c1_bitwise(P):
             assert np.array_equal(a.get_state(w), g.get_state(w)), (u, w)
 
 
+def test_graph_direct_c1_misaligned_buffer(P):
+    """the c = 1 direct graph path reads the producer's buffer with 256-bit loads, so a buffer that is not
+    32-byte aligned (a view at an odd element offset) must take the accumulate path instead -- same bits, no fault."""
+    import torch
+    wl = models.Workload("direct_mis", [("w", 100_003, 0)], 1, 1)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    a = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, fuse_final=0))
+    g = P.UpdateStep(wl.numel, theta0, lib_cfg(wl, fuse_final=0))
+    big = torch.empty(lay.n + 1, dtype=torch.int16, device="cuda")
+    buf = big[1:]                                   # 2-byte aligned only
+    assert buf.data_ptr() % 32 != 0
+    g.graph_capture([buf])
+    for u in range(1, 4):
+        x = synth.micro_grad_cpu(wl, lay, u, 0, 1, 7)
+        tok = synth.ntokens(wl, u, 0, 1)
+        a.accumulate(h2t(x), tok)
+        ra = a.step()
+        buf.copy_(h2t(x))
+        g.graph_launch([tok])
+        assert decisions(g.result(u)) == decisions(ra), u
+        for w in (0, 1, 2, 3):
+            assert np.array_equal(a.get_state(w), g.get_state(w)), (u, w)
+
+
+def test_result_of_restored_attempt_is_einval(P):
+    """after set_state(SCALARS) the result ring holds none of the restored attempts: smpu_result for
+    them is EINVAL instead of a stale record; attempts run after the restore are served."""
+    import torch
+    wl = models.Workload("ring", [("w", 10_000, 0)], 1, 1)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    st = P.UpdateStep(wl.numel, theta0, lib_cfg(wl))
+    g = torch.zeros(lay.n, dtype=torch.int16, device="cuda")
+    st.set_state(P.smpu.STATE_SCALARS, np.array([7, 3, 40, 50], dtype=np.int64))
+    for attempt in (1, 50):
+        with pytest.raises(P.SmpuError) as ei:
+            st.result(attempt)
+        assert ei.value.status == P.smpu.EINVAL
+    st.accumulate(g, 100)
+    st.step(wait=False)
+    r = st.result(51)
+    assert r["attempt"] == 51 and r["num_updates"] == 41 and r["applied"] == 1
+    st.close()
+
+
 def test_real_training_loop_example(P):
     """examples/train_tiny.py: a real fp16 model whose weights are views of the library's w16, loss scaled by the
     library's device scale, update by libsmpu -- the loss must fall from ln V towards the 10%-noise floor."""
