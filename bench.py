@@ -50,6 +50,9 @@ def parse():
                     help="smpu_config.ar_pieces (replicated, W > 1): the last bucket's all-reduce in pieces, "
                          "each followed by its Adam; default: the library's")
     ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
+    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1], default=0,
+                    help="smpu_config.ar_copy_engine (replicated, W > 1): the bucket all-reduce's NVLink traffic by "
+                         "the copy engines (cudaMemcpyAsync push + all-gather, SM fold only)")
     ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
                     help="input family (SURVEY 8(d.2)); real_sparse = G_real with the row-sparse embedding gradient "
                          "(Zipf(1.1) token rows); the performance-independence check times all four")
@@ -237,6 +240,7 @@ def bench_config(args, wl, world, toks_per_update, path_bytes_per_elem, sharded=
             "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
             "path_bytes_per_elem": path_bytes_per_elem,
             "optimizer": "sharded (SURVEY f2)" if (sharded and world > 1) else "replicated (paper)",
+            "ar_copy_engine": int(getattr(args, "ar_copy_engine", 0)),
             "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"}
 
 
@@ -779,6 +783,8 @@ def main_ours(args):
                                ar_ctas=args.ar_ctas)
         if args.ar_pieces is not None:
             cfg.ar_pieces = args.ar_pieces
+        if not sharded:
+            cfg.ar_copy_engine = args.ar_copy_engine
         # growth interval beyond the run: the scale stays at 2^7, so the pre-generated inputs stay valid
         cfg.growth_interval = 1 << 40
         return cfg

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SMPU_ABI_VERSION 3
+#define SMPU_ABI_VERSION 4
 #define SMPU_NCCL_ID_BYTES 128
 
 typedef struct smpu_ctx smpu_ctx;
@@ -106,6 +106,12 @@ typedef struct {
                                   starts after the first piece rather than the first whole bucket and the two
                                   pipeline.  1 (default) = one launch per bucket; 1..64.  Collective: compared across
                                   ranks like the ar_* fields.                                                        */
+    int32_t ar_copy_engine;    /* world > 1, fused all-reduce, replicated layout: 0 (default) = SM peer loads / stores
+                                  (k_ar32); 1 = the NVLink traffic moved by the copy engines (one cudaMemcpyAsync per
+                                  peer for the reduce-scatter push and the all-gather, an SM kernel only for the local
+                                  ascending-rank fold), so a bucket in flight holds no SM while a backward or K1 runs.
+                                  Same bits.  The window grows by ~2 B per parameter of staging.  EINVAL with sharded,
+                                  ar_mcast or SMPU_AR_NCCL.  Collective: compared across ranks.                       */
 } smpu_config;
 
 /* bucket all-reduce implementations (smpu_config.allreduce, smpu_allreduce_impl) */

@@ -227,6 +227,61 @@ __global__ void __launch_bounds__(512) k_ar32(Peers pe, int64_t lo, int64_t hi) 
     pe.sync(pe.cta());
 }
 
+// ------------------------------------------------------------------- copy-engine variant (smpu_config.ar_copy_engine)
+// The same reduce-scatter + all-gather with the NVLink traffic moved by the copy engines instead of SM loads and
+// stores, so the bucket all-reduce holds no SM while the data crosses the fabric (a running backward or K1 keeps
+// every SM).  Shards as in k_ar32 (16-element units, ceil(units / W) per rank).  Per bucket, on rank r:
+//   1. push: one cudaMemcpyAsync per peer p of r's contribution to shard p into p's staging slot r (window offset
+//      stage_off + r * per * 32 B), issued from r's copy streams (NVLink writes);
+//   2. k_ce_barrier: every rank's pushes of this bucket have completed (a stream runs the barrier kernel only after
+//      its copies are done);
+//   3. k_ce_reduce: R of shard r = the ascending-rank fold of the W contributions (slot s, or r's own accumulator
+//      for s = r) with an rn16 add after each term -- the order of k_ar32 and of the oracle (reading R3) -- stored
+//      into r's accumulator; rank 0 also does the unaligned head / tail over peer memory as k_ar32 does;
+//   4. all-gather: one cudaMemcpyAsync per peer of R's shard r into p's accumulator;
+//   5. k_ce_barrier: every rank's all-gather has landed before anything reads the accumulator.
+// Bits are identical to k_ar32's (same fold, same order).  LocalPeers (virtual ranks): the same copies between the
+// local windows, one k_ce_reduce launch for every rank, and stream order instead of the two barriers.
+template <class Peers>
+__global__ void k_ce_barrier(Peers pe, uint32_t idx) {
+    pe.sync(idx);
+}
+
+template <class Peers>
+__global__ void k_peer_ptrs(Peers pe, int W, unsigned long long* out) {
+    if ((int)threadIdx.x < W) out[threadIdx.x] = (unsigned long long)(uintptr_t)pe.at((int)threadIdx.x, 0);
+}
+
+template <int W, class Peers>
+__global__ void __launch_bounds__(256) k_ce_reduce(Peers pe, int64_t lo, int64_t hi, size_t stage_off) {
+    uint16_t* base[W];
+#pragma unroll
+    for (int p = 0; p < W; ++p) base[p] = (uint16_t*)pe.at(p, 0);
+    const int me = pe.rank();
+    const int64_t v0 = (lo + 15) & ~(int64_t)15, v1 = hi & ~(int64_t)15;
+    const int64_t units = v1 > v0 ? (v1 - v0) / 16 : 0;
+    const int64_t per = (units + W - 1) / W;
+    int64_t u_lo = me * per, u_hi = u_lo + per;
+    if (u_lo > units) u_lo = units;
+    if (u_hi > units) u_hi = units;
+    const uint16_t* stage = (const uint16_t*)pe.at(me, stage_off);   // slot s at stage + s * per * 16
+    uint16_t* acc = base[me];
+    const int64_t tid = (int64_t)pe.cta() * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)pe.ctas() * blockDim.x;
+    for (int64_t u = u_lo + tid; u < u_hi; u += nthr) {
+        const int64_t i0 = v0 + u * 16, j0 = (u - u_lo) * 16;
+        V8 a[W];
+#pragma unroll
+        for (int s = 0; s < W; ++s) a[s] = s == me ? ld256(acc + i0) : ld256_ro(stage + s * per * 16 + j0);
+#pragma unroll
+        for (int s = 1; s < W; ++s)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[0].w[j] = hadd2_rn(a[0].w[j], a[s].w[j]);
+        st256(acc + i0, a[0]);
+    }
+    if (me == 0) head_tail<W, true>(base, lo, hi, v0, v1, tid, nthr);
+}
+
 // --------------------------------------------------------------------------------------- decision exchange
 // Per-rank arguments of the decision kernels.  An LsaPeers launch fills r[its rank]; a LocalPeers launch fills
 // every virtual rank's (the kernel indexes r[pe.rank()]).

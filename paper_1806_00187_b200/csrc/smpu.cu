@@ -94,6 +94,13 @@ struct smpu_ctx {
     bool ar_vec32 = false;                                  // 256-bit peer accesses in the fused all-reduce
     bool ar_mcast = false;                                  // all-gather by NVLS multicast stores
     int ar_unroll = 1, ar_threads = 256;                    // fused all-reduce shape (smpu_config.ar_*)
+    // copy-engine all-reduce (smpu_config.ar_copy_engine): staging offset in the window of every piece, every rank's
+    // window as a VA of this process (LSA peers; the copies' destinations), W - 1 copy streams and their events
+    bool ce = false;
+    std::vector<std::vector<size_t>> ce_off;
+    char* peer_win[kMaxLsaRanks] = {};
+    cudaStream_t ce_stream[kMaxLsaRanks] = {};
+    cudaEvent_t ce_fork = nullptr, ce_join[kMaxLsaRanks] = {};
     smpu_group* group = nullptr;                            // virtual rank of a one-GPU group (smpu_group_init)
     bool w16_in_win = false;                                // w16 is a slice of the window allocation
     cudaStream_t step_stream = nullptr;                     // group, sharded: the stream of the deferred tail
@@ -564,6 +571,105 @@ smpu_status launch_ar_fused(smpu_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
     return launch_ar_with(ctx, lsa_peers(ctx), ctx->grid_ar, lo, hi, cs);
 }
 
+// Copy-engine all-reduce (smpu_config.ar_copy_engine; lsa_allreduce.cuh "copy-engine variant"): shard p of
+// [lo, hi) is [v0 + u_lo(p) * 16, v0 + u_hi(p) * 16) in k_ar32's 16-element units; staging slot s of a piece is at
+// window offset stage_off + s * per * 32.
+struct CeGeom {
+    int64_t v0 = 0, units = 0, per = 0;
+    CeGeom(int64_t lo, int64_t hi, int W) {
+        v0 = (lo + 15) & ~(int64_t)15;
+        const int64_t v1 = hi & ~(int64_t)15;
+        units = v1 > v0 ? (v1 - v0) / 16 : 0;
+        per = (units + W - 1) / W;
+    }
+    int64_t ulo(int p) const { return p * per < units ? p * per : units; }
+    int64_t uhi(int p) const { return (p + 1) * per < units ? (p + 1) * per : units; }
+};
+
+// Copies issued on the ctx's W - 1 copy streams forked from / joined into `cs`: copy j goes to `dst(j)` from
+// `src(j)`, `bytes(j)` bytes (skipped when 0).
+template <class F>
+smpu_status ce_copies(smpu_ctx* ctx, int count, cudaStream_t cs, F&& one) {
+    CK(cudaEventRecord(ctx->ce_fork, cs));
+    for (int j = 0; j < count; ++j) {
+        cudaStream_t st = ctx->ce_stream[j % (ctx->world - 1)];
+        CK(cudaStreamWaitEvent(st, ctx->ce_fork, 0));
+        void* dst = nullptr;
+        const void* src = nullptr;
+        size_t bytes = 0;
+        one(j, dst, src, bytes);
+        if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+        CK(cudaEventRecord(ctx->ce_join[j % (ctx->world - 1)], st));
+        CK(cudaStreamWaitEvent(cs, ctx->ce_join[j % (ctx->world - 1)], 0));
+    }
+    return SMPU_OK;
+}
+
+smpu_status launch_ar_ce(smpu_ctx* ctx, int64_t lo, int64_t hi, size_t stage_off, cudaStream_t cs) {
+    const int W = ctx->world, r = ctx->rank;
+    const CeGeom G(lo, hi, W);
+    const LsaPeers pe = lsa_peers(ctx);
+    uint16_t* acc = ctx->acc;
+    // 1. push my contribution to shard p into p's staging slot r
+    smpu_status st = ce_copies(ctx, W - 1, cs, [&](int j, void*& dst, const void*& src, size_t& bytes) {
+        const int p = (r + 1 + j) % W;
+        dst = ctx->peer_win[p] + stage_off + (size_t)r * G.per * 32;
+        src = acc + G.v0 + G.ulo(p) * 16;
+        bytes = (size_t)(G.uhi(p) - G.ulo(p)) * 32;
+    });
+    if (st != SMPU_OK) return st;
+    // 2. every rank's pushes have landed; 3. fold my shard (+ rank 0: head / tail over peer memory)
+    k_ce_barrier<LsaPeers><<<1, 32, 0, cs>>>(pe, 0);
+    CKL("k_ce_barrier");
+#define SMPU_CER(WW) k_ce_reduce<WW, LsaPeers><<<ctx->grid_ar, 256, 0, cs>>>(pe, lo, hi, stage_off)
+    SMPU_BY_WORLD(W, SMPU_CER, "copy-engine all-reduce")
+#undef SMPU_CER
+    CKL("k_ce_reduce");
+    // 4. all-gather R of my shard into every peer's accumulator; 5. every rank's all-gather has landed
+    st = ce_copies(ctx, W - 1, cs, [&](int j, void*& dst, const void*& src, size_t& bytes) {
+        const int p = (r + 1 + j) % W;
+        const int64_t off = G.v0 + G.ulo(r) * 16;
+        dst = ctx->peer_win[p] + (size_t)off * 2;
+        src = acc + off;
+        bytes = (size_t)(G.uhi(r) - G.ulo(r)) * 32;
+    });
+    if (st != SMPU_OK) return st;
+    k_ce_barrier<LsaPeers><<<1, 32, 0, cs>>>(pe, 1);
+    CKL("k_ce_barrier");
+    ctx->launches[SMPU_ALLREDUCE] += 2;   // three kernels; the caller's Timed counted one
+    return SMPU_OK;
+}
+
+// The same over the W windows of a virtual group, on the group's comm stream: the copies between local windows
+// (issued through the issuing member's copy streams), one fold launch for every rank, stream order for barriers.
+smpu_status launch_ar_ce_group(smpu_ctx* ctx, int64_t lo, int64_t hi, size_t stage_off, cudaStream_t cs) {
+    smpu_group* g = ctx->group;
+    const int W = g->world;
+    const CeGeom G(lo, hi, W);
+    char* win[kMaxLsaRanks];
+    for (int p = 0; p < W; ++p) win[p] = (char*)g->m[p]->acc;
+    // pushes: (r, p) for every ordered pair, rank-major
+    smpu_status st = ce_copies(ctx, W * (W - 1), cs, [&](int j, void*& dst, const void*& src, size_t& bytes) {
+        const int r = j / (W - 1), p = (r + 1 + j % (W - 1)) % W;
+        dst = win[p] + stage_off + (size_t)r * G.per * 32;
+        src = win[r] + (size_t)(G.v0 + G.ulo(p) * 16) * 2;
+        bytes = (size_t)(G.uhi(p) - G.ulo(p)) * 32;
+    });
+    if (st != SMPU_OK) return st;
+    const LocalPeers pe = local_peers(g, g->per_rank, 0);
+#define SMPU_CER(WW) k_ce_reduce<WW, LocalPeers><<<g->per_rank * W, 256, 0, cs>>>(pe, lo, hi, stage_off)
+    SMPU_BY_WORLD(W, SMPU_CER, "copy-engine all-reduce")
+#undef SMPU_CER
+    CKL("k_ce_reduce (virtual)");
+    return ce_copies(ctx, W * (W - 1), cs, [&](int j, void*& dst, const void*& src, size_t& bytes) {
+        const int r = j / (W - 1), p = (r + 1 + j % (W - 1)) % W;
+        const size_t off = (size_t)(G.v0 + G.ulo(r) * 16) * 2;
+        dst = win[p] + off;
+        src = win[r] + off;
+        bytes = (size_t)(G.uhi(r) - G.ulo(r)) * 32;
+    });
+}
+
 smpu_status launch_k1_many(smpu_ctx* ctx, const uint16_t* const* g, int count, int64_t lo, int64_t hi, bool first,
                            bool detect, bool stats, cudaStream_t s) {
     if (hi <= lo) return SMPU_OK;
@@ -598,7 +704,10 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
         for (size_t i = 0; i + 1 < pc.size(); ++i) {
             {
                 Timed t(ctx, SMPU_ALLREDUCE, cs);
-                if (ctx->ar_impl == SMPU_AR_FUSED) {
+                if (ctx->ce) {
+                    smpu_status st = launch_ar_ce(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], cs);
+                    if (st != SMPU_OK) return st;
+                } else if (ctx->ar_impl == SMPU_AR_FUSED) {
                     smpu_status st = launch_ar_fused(ctx, pc[i], pc[i + 1], cs);
                     if (st != SMPU_OK) return st;
                 } else {
@@ -624,8 +733,9 @@ smpu_status group_issue_buckets(smpu_ctx* ctx) {
         for (smpu_ctx* q : g->m) CK(cudaStreamWaitEvent(g->comm, q->ready[b], 0));
         const auto& pc = ctx->pieces[b];
         for (size_t i = 0; i + 1 < pc.size(); ++i) {
-            smpu_status st = launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world, pc[i],
-                                            pc[i + 1], g->comm);
+            smpu_status st = ctx->ce ? launch_ar_ce_group(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], g->comm)
+                                     : launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world,
+                                                      pc[i], pc[i + 1], g->comm);
             if (st != SMPU_OK) return st;
             for (smpu_ctx* q : g->m) {
                 q->launches[SMPU_ALLREDUCE]++;
@@ -908,6 +1018,10 @@ smpu_status check_cfg(const smpu_config* c) {
                                     "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1, ar_pieces 1..64");
     if (c->ar_mcast && c->ar_vec_bytes != 32)
         return set_err(SMPU_EINVAL, "ar_mcast needs ar_vec_bytes = 32");
+    if (c->ar_copy_engine != 0 && c->ar_copy_engine != 1) return set_err(SMPU_EINVAL, "ar_copy_engine must be 0|1");
+    if (c->ar_copy_engine && (c->sharded || c->ar_mcast || c->allreduce == SMPU_AR_NCCL))
+        return set_err(SMPU_EINVAL, "ar_copy_engine runs the replicated fused all-reduce only (not with sharded, "
+                                    "ar_mcast or SMPU_AR_NCCL)");
     return SMPU_OK;
 }
 
@@ -955,6 +1069,9 @@ void free_ctx(smpu_ctx* c) {
     if (c->comm_done) cudaEventDestroy(c->comm_done);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    for (auto& x : c->ce_stream) if (x) cudaStreamDestroy(x);
+    for (auto& e : c->ce_join) if (e) cudaEventDestroy(e);
+    if (c->ce_fork) cudaEventDestroy(c->ce_fork);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     cudaFree(c->tok_dev);
@@ -1004,6 +1121,7 @@ smpu_status smpu_config_default(smpu_config* c) {
     c->ar_mcast = 0;
     c->pdl = 1;
     c->ar_pieces = 1;
+    c->ar_copy_engine = 0;
     return SMPU_OK;
 }
 
@@ -1148,14 +1266,50 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         IK(cudaMalloc(&ctx->v_b, n * 4));
     }
 
+    // all-reduce pieces: with ar_pieces = P (replicated layout, world > 1) every bucket is cut into P pieces on
+    // 256-element boundaries, each all-reduced and then updated on its own, so that Adam of piece i overlaps the
+    // all-reduce of piece i + 1 and the Adam chain starts after the first piece instead of the first bucket.  Values
+    // never change (elementwise).
+    ctx->pieces.resize(ctx->nb);
+    ctx->ar_done.resize(ctx->nb);
+    for (int b = 0; b < ctx->nb; ++b) {
+        const int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
+        const int split = (!cfg->sharded && world > 1) ? cfg->ar_pieces : 1;
+        auto& pc = ctx->pieces[b];
+        pc.push_back(lo);
+        const int64_t step = (hi - lo + split - 1) / split;
+        for (int i = 1; i < split; ++i) {
+            const int64_t cut = (lo + i * step + 255) & ~(int64_t)255;
+            if (cut > pc.back() && cut < hi) pc.push_back(cut);
+        }
+        pc.push_back(hi);
+        ctx->ar_done[b].assign(pc.size() - 1, nullptr);
+        for (auto& e : ctx->ar_done[b]) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     const size_t acc_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
     const size_t w16_bytes = ((size_t)n * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
                              NCCL_WIN_REQUIRED_ALIGNMENT;
-    // window = [acc | w16 | decision area (early + late exchange slots: 2 parities x 8 ranks x 16 B each)]
-    const size_t win_bytes = acc_bytes + w16_bytes + NCCL_WIN_REQUIRED_ALIGNMENT;
+    // window = [acc | w16 | decision area (early + late exchange slots: 2 parities x 8 ranks x 16 B each) |
+    //           copy-engine staging (ar_copy_engine: per piece, W slots of one shard each)]
     ctx->w16_off = acc_bytes;
     ctx->dec_area_off = acc_bytes + w16_bytes;
+    size_t win_bytes = acc_bytes + w16_bytes + NCCL_WIN_REQUIRED_ALIGNMENT;
+    ctx->ce = world > 1 && cfg->ar_copy_engine != 0;
+    if (ctx->ce) {
+        ctx->ce_off.resize(ctx->nb);
+        for (int b = 0; b < ctx->nb; ++b) {
+            const auto& pc = ctx->pieces[b];
+            for (size_t i = 0; i + 1 < pc.size(); ++i) {
+                const int64_t v0 = (pc[i] + 15) & ~(int64_t)15, v1 = pc[i + 1] & ~(int64_t)15;
+                const int64_t units = v1 > v0 ? (v1 - v0) / 16 : 0, per = (units + world - 1) / world;
+                ctx->ce_off[b].push_back(win_bytes);
+                win_bytes += ((size_t)world * per * 32 + 255) & ~(size_t)255;
+            }
+        }
+        win_bytes = (win_bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
+                    NCCL_WIN_REQUIRED_ALIGNMENT;
+    }
     if (cfg->sharded && world > 1 && cfg->allreduce == SMPU_AR_NCCL)
         return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce"));
     if (group) {
@@ -1186,26 +1340,6 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
     for (auto& e : ctx->ring_ev) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->ready.resize(ctx->nb);
     for (auto& e : ctx->ready) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    // all-reduce pieces: with ar_pieces = P (replicated layout, world > 1) every bucket is cut into P pieces on
-    // 256-element boundaries, each all-reduced and then updated on its own, so that Adam of piece i overlaps the
-    // all-reduce of piece i + 1 and the Adam chain starts after the first piece instead of the first bucket.  Values
-    // never change (elementwise).
-    ctx->pieces.resize(ctx->nb);
-    ctx->ar_done.resize(ctx->nb);
-    for (int b = 0; b < ctx->nb; ++b) {
-        const int64_t lo = ctx->bbegin[b], hi = ctx->bbegin[b + 1];
-        const int split = (!cfg->sharded && world > 1) ? cfg->ar_pieces : 1;
-        auto& pc = ctx->pieces[b];
-        pc.push_back(lo);
-        const int64_t step = (hi - lo + split - 1) / split;
-        for (int i = 1; i < split; ++i) {
-            const int64_t cut = (lo + i * step + 255) & ~(int64_t)255;
-            if (cut > pc.back() && cut < hi) pc.push_back(cut);
-        }
-        pc.push_back(hi);
-        ctx->ar_done[b].assign(pc.size() - 1, nullptr);
-        for (auto& e : ctx->ar_done[b]) IK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
     IK(cudaEventCreateWithFlags(&ctx->dec_ev, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->k2_done, cudaEventDisableTiming));
     IK(cudaEventCreateWithFlags(&ctx->tail_ev, cudaEventDisableTiming));
@@ -1286,11 +1420,11 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         // window registration or in LSA barriers the others never join.  EINVAL on every rank instead.
         static const char* kField[] = {"update_freq", "bucket_bytes", "split_tensors", "sharded", "accum_fp32",
                                        "allreduce", "ar_ctas", "ar_threads", "ar_vec_bytes", "ar_unroll", "ar_mcast",
-                                       "ar_pieces", "n (parameter count)", "n_buckets",
+                                       "ar_pieces", "ar_copy_engine", "n (parameter count)", "n_buckets",
                                        "symmetric-memory allocation"};
         const int64_t mine[] = {cfg->update_freq, cfg->bucket_bytes, cfg->split_tensors, cfg->sharded,
                                 cfg->accum_fp32, cfg->allreduce, ctx->grid_ar, cfg->ar_threads, cfg->ar_vec_bytes,
-                                cfg->ar_unroll, cfg->ar_mcast, cfg->ar_pieces, n, ctx->nb,
+                                cfg->ar_unroll, cfg->ar_mcast, cfg->ar_pieces, cfg->ar_copy_engine, n, ctx->nb,
                                 ctx->acc_from_nccl ? 1 : 0};
         constexpr int K = sizeof(mine) / sizeof(mine[0]);
         int64_t mn[K], mx[K];
@@ -1333,6 +1467,27 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         ctx->sharded = cfg->sharded && ctx->ar_impl == SMPU_AR_FUSED;
         if (cfg->sharded && !ctx->sharded)
             return bail(set_err(SMPU_EINVAL, "the sharded optimizer needs the fused all-reduce (unavailable)"));
+        if (ctx->ce && ctx->ar_impl != SMPU_AR_FUSED)
+            return bail(set_err(SMPU_EINVAL, "ar_copy_engine needs the fused all-reduce's window (unavailable)"));
+        if (ctx->ce) {
+            // every rank's window as a VA of this process: the copy engines' push / all-gather destinations
+            unsigned long long* d = nullptr;
+            unsigned long long h[kMaxLsaRanks] = {};
+            IK(cudaMalloc(&d, sizeof h));
+            k_peer_ptrs<LsaPeers><<<1, 32, 0, s0>>>(lsa_peers(ctx), world, d);
+            IK(cudaGetLastError());
+            IK(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, s0));
+            IK(cudaStreamSynchronize(s0));
+            IK(cudaFree(d));
+            for (int p = 0; p < world; ++p) ctx->peer_win[p] = (char*)(uintptr_t)h[p];
+        }
+    }
+    if (ctx->ce) {
+        IK(cudaEventCreateWithFlags(&ctx->ce_fork, cudaEventDisableTiming));
+        for (int j = 0; j + 1 < world; ++j) {
+            IK(cudaStreamCreateWithPriority(&ctx->ce_stream[j], cudaStreamNonBlocking, hi_prio));
+            IK(cudaEventCreateWithFlags(&ctx->ce_join[j], cudaEventDisableTiming));
+        }
     }
     if (ctx->sharded) {
         // the same shard split as k_rs: 8-element units, ceil(units / W) per rank, rank 0 also owns the bucket's

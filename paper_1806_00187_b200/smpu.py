@@ -42,7 +42,7 @@ class Config(ctypes.Structure):
                 ("fuse_final", ctypes.c_int32), ("accum_fp32", ctypes.c_int32), ("split_tensors", ctypes.c_int32),
                 ("ar_ctas", ctypes.c_int32), ("ar_threads", ctypes.c_int32), ("ar_vec_bytes", ctypes.c_int32),
                 ("ar_unroll", ctypes.c_int32), ("ar_mcast", ctypes.c_int32), ("pdl", ctypes.c_int32),
-                ("ar_pieces", ctypes.c_int32)]
+                ("ar_pieces", ctypes.c_int32), ("ar_copy_engine", ctypes.c_int32)]
 
 
 class StepResult(ctypes.Structure):

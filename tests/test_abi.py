@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(P):
 
 
 def test_abi_version_and_defaults(P):
-    assert P.abi_version() == 3
+    assert P.abi_version() == 4
     c = P.config_default()
     # fuse_final is opt-in: the default ctx keeps SURVEY 8(b)'s contract (w16 changes only inside smpu_step)
     assert (c.allreduce, c.sharded, c.fuse_final, c.accum_fp32, c.split_tensors) == (0, 0, 0, 0, 0)
@@ -47,6 +47,7 @@ def test_abi_version_and_defaults(P):
     assert c.bucket_bytes == 150 << 20                                                                # P:212 fn
     # the fused all-reduce's shape lives in the config (compared across ranks at init), not in the environment
     assert (c.ar_ctas, c.ar_threads, c.ar_vec_bytes, c.ar_unroll, c.ar_mcast, c.pdl) == (0, 256, 32, 1, 0, 1)
+    assert (c.ar_pieces, c.ar_copy_engine) == (1, 0)
 
 
 def test_library_reads_no_environment_knobs():
@@ -197,7 +198,8 @@ def test_config_and_group_argument_errors_need_no_gpu(P):
     wl = models.Workload("args", [("w", 1000, 0)], 1, 1)
     theta0 = np.zeros(1000, np.float32)
     for bad in (dict(ar_threads=300), dict(ar_vec_bytes=8), dict(ar_unroll=3), dict(ar_ctas=-1), dict(pdl=2),
-                dict(ar_mcast=1, ar_vec_bytes=16)):
+                dict(ar_mcast=1, ar_vec_bytes=16), dict(ar_copy_engine=2), dict(ar_copy_engine=1, sharded=1),
+                dict(ar_copy_engine=1, ar_mcast=1), dict(ar_copy_engine=1, allreduce=P.smpu.AR_NCCL)):
         with pytest.raises(P.SmpuError) as ei:
             P.UpdateStep(wl.numel, theta0, P.config_default(**bad))
         assert ei.value.status == P.smpu.EINVAL, bad

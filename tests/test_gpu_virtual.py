@@ -158,6 +158,15 @@ def test_virtual_pieces(world, split):
     _run(world, "real", False, mode="buckets", ar_pieces=split)
 
 
+@pytest.mark.parametrize("world,mode,split", [(2, "calls", 1), (3, "buckets", 1), (4, "calls", 3), (8, "buckets", 1),
+                                              (5, "many", 2)])
+def test_virtual_copy_engine(world, mode, split):
+    """smpu_config.ar_copy_engine: the bucket all-reduce's traffic moved by cudaMemcpyAsync (push of every shard to
+    its owner's staging, fold, all-gather of R): decisions and R bitwise the oracle's (the fold is k_ar32's
+    ascending-rank order), alone and with ar_pieces, through every injection kind."""
+    _run(world, "real", False, mode=mode, ar_copy_engine=1, ar_pieces=split)
+
+
 @pytest.mark.parametrize("world,sharded", [(4, False), (7, True)])
 def test_virtual_accumulate_many(world, sharded):
     _run(world, "real", sharded, mode="many")
