@@ -50,9 +50,10 @@ def parse():
                     help="smpu_config.ar_pieces (replicated, W > 1): the last bucket's all-reduce in pieces, "
                          "each followed by its Adam; default: the library's")
     ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
-    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1], default=0,
+    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1, 2], default=0,
                     help="smpu_config.ar_copy_engine (replicated, W > 1): the bucket all-reduce's NVLink traffic by "
-                         "the copy engines (cudaMemcpyAsync push + all-gather, SM fold only)")
+                         "the copy engines (cudaMemcpyAsync push + all-gather, SM fold only); 2: all buckets but the "
+                         "last")
     ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
                     help="input family (SURVEY 8(d.2)); real_sparse = G_real with the row-sparse embedding gradient "
                          "(Zipf(1.1) token rows); the performance-independence check times all four")

@@ -109,8 +109,9 @@ typedef struct {
     int32_t ar_copy_engine;    /* world > 1, fused all-reduce, replicated layout: 0 (default) = SM peer loads / stores
                                   (k_ar32); 1 = the NVLink traffic moved by the copy engines (one cudaMemcpyAsync per
                                   peer for the reduce-scatter push and the all-gather, an SM kernel only for the local
-                                  ascending-rank fold), so a bucket in flight holds no SM while a backward or K1 runs.
-                                  Same bits.  The window grows by ~2 B per parameter of staging.  EINVAL with sharded,
+                                  ascending-rank fold), so a bucket in flight holds no SM while a backward or K1 runs;
+                                  2 = the copy engines for every bucket but the last, which is ready only once the
+                                  backward has ended and goes through the SM kernel (higher bandwidth).  Same bits.  The window grows by ~2 B per parameter of staging.  EINVAL with sharded,
                                   ar_mcast or SMPU_AR_NCCL.  Collective: compared across ranks.                       */
 } smpu_config;
 

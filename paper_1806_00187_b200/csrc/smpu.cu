@@ -586,6 +586,10 @@ struct CeGeom {
     int64_t uhi(int p) const { return (p + 1) * per < units ? (p + 1) * per : units; }
 };
 
+// ar_copy_engine 1: every bucket on the copy engines; 2: every bucket but the last (the last one is ready only when
+// the backward has ended, so nothing is left to overlap it with and k_ar32's higher in-situ bandwidth wins)
+bool ce_bucket(const smpu_ctx* ctx, int b) { return ctx->ce && (ctx->cfg.ar_copy_engine == 1 || b + 1 < ctx->nb); }
+
 // Copies issued on the ctx's W - 1 copy streams forked from / joined into `cs`: copy j goes to `dst(j)` from
 // `src(j)`, `bytes(j)` bytes (skipped when 0).
 template <class F>
@@ -704,7 +708,7 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
         for (size_t i = 0; i + 1 < pc.size(); ++i) {
             {
                 Timed t(ctx, SMPU_ALLREDUCE, cs);
-                if (ctx->ce) {
+                if (ce_bucket(ctx, b)) {
                     smpu_status st = launch_ar_ce(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], cs);
                     if (st != SMPU_OK) return st;
                 } else if (ctx->ar_impl == SMPU_AR_FUSED) {
@@ -733,7 +737,7 @@ smpu_status group_issue_buckets(smpu_ctx* ctx) {
         for (smpu_ctx* q : g->m) CK(cudaStreamWaitEvent(g->comm, q->ready[b], 0));
         const auto& pc = ctx->pieces[b];
         for (size_t i = 0; i + 1 < pc.size(); ++i) {
-            smpu_status st = ctx->ce ? launch_ar_ce_group(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], g->comm)
+            smpu_status st = ce_bucket(ctx, b) ? launch_ar_ce_group(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], g->comm)
                                      : launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world,
                                                       pc[i], pc[i + 1], g->comm);
             if (st != SMPU_OK) return st;
@@ -1018,7 +1022,7 @@ smpu_status check_cfg(const smpu_config* c) {
                                     "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1, ar_pieces 1..64");
     if (c->ar_mcast && c->ar_vec_bytes != 32)
         return set_err(SMPU_EINVAL, "ar_mcast needs ar_vec_bytes = 32");
-    if (c->ar_copy_engine != 0 && c->ar_copy_engine != 1) return set_err(SMPU_EINVAL, "ar_copy_engine must be 0|1");
+    if (c->ar_copy_engine < 0 || c->ar_copy_engine > 2) return set_err(SMPU_EINVAL, "ar_copy_engine must be 0|1|2");
     if (c->ar_copy_engine && (c->sharded || c->ar_mcast || c->allreduce == SMPU_AR_NCCL))
         return set_err(SMPU_EINVAL, "ar_copy_engine runs the replicated fused all-reduce only (not with sharded, "
                                     "ar_mcast or SMPU_AR_NCCL)");

@@ -34,14 +34,15 @@ def test_world2(family, impl):
     _run(2, family, port=29531 + (family == "real") + 2 * (impl == "fused"), impl=impl)
 
 
-@pytest.mark.parametrize("world,graph", [(2, False), (2, True), (4, False), (4, True)])
-def test_copy_engine_allreduce(world, graph):
+@pytest.mark.parametrize("world,graph,ce", [(2, False, 1), (2, True, 1), (4, False, 1), (4, True, 1), (2, True, 2),
+                                            (4, False, 2)])
+def test_copy_engine_allreduce(world, graph, ce):
     """smpu_config.ar_copy_engine over real NVLink peers: pushes and all-gathers by cudaMemcpyAsync into the other
     ranks' NCCL windows, LSA barriers, the ascending-rank fold; decisions and R bitwise the oracle's (G_real, every
     injection kind), call by call and as one CUDA graph per update."""
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
-    _run(world, "real", port=29581 + 2 * world + graph, impl="ce", graph=graph)
+    _run(world, "real", port=29581 + 2 * world + graph + 8 * (ce - 1), impl="ce" if ce == 1 else "ce2", graph=graph)
 
 
 @pytest.mark.parametrize("impl", ["nccl", "fused"])
