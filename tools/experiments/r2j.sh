@@ -7,6 +7,8 @@ set -x
 O=gpurun_out/r2j_w$W
 mkdir -p $O
 cat .head_sha > $O/head.txt
+timeout 300 ./tools/nvlink_probe 512 > $O/nvlink_probe.jsonl 2> $O/nvlink_probe.err
+timeout 300 python tools/ce_probe.py 256 > $O/ce_probe.jsonl 2> $O/ce_probe.err
 timeout 900 python -m pytest tests/test_gpu_virtual.py -q -k copy_engine > $O/virtual_ce.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_multi.py -v -k copy_engine > $O/multi_ce.log 2>&1
 for ce in 0 1 2; do
