@@ -47,13 +47,15 @@ def parse():
                          "with the sharded variant timed beside it when the fused all-reduce is available")
     ap.add_argument("--sharded", action="store_true", help="same as --optimizer sharded")
     ap.add_argument("--ar-pieces", type=int, default=None,
-                    help="smpu_config.ar_pieces (replicated, W > 1): the last bucket's all-reduce in pieces, "
-                         "each followed by its Adam; default: the library's")
+                    help="smpu_config.ar_pieces (replicated, W > 1): every bucket's all-reduce in pieces, "
+                         "each followed by its Adam; default 2 (measured best or equal at W = 2 / 4, c = 16 / 1: "
+                         "profiles/r2/f_w4/c4_w4_pieces.jsonl)")
     ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
-    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1, 2], default=0,
+    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1, 2], default=None,
                     help="smpu_config.ar_copy_engine (replicated, W > 1): the bucket all-reduce's NVLink traffic by "
                          "the copy engines (cudaMemcpyAsync push + all-gather, SM fold only); 2: all buckets but the "
-                         "last")
+                         "last.  Default: 0 in m1 (the HBM-bound update step alone: the SM kernel moves the fewest "
+                         "HBM bytes), 1 in m2 / train (a backward runs beside the exchange: keep its SMs)")
     ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
                     help="input family (SURVEY 8(d.2)); real_sparse = G_real with the row-sparse embedding gradient "
                          "(Zipf(1.1) token rows); the performance-independence check times all four")
@@ -87,7 +89,12 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline leg")
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: oracle seconds for the whole run, spread over the steps")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.ar_copy_engine is None:
+        args.ar_copy_engine = 0 if args.mode == "m1" else 1
+    if args.ar_pieces is None:
+        args.ar_pieces = 2 if args.gpus > 1 else 1
+    return args
 
 
 def set_generator(wl, generator):
@@ -241,7 +248,7 @@ def bench_config(args, wl, world, toks_per_update, path_bytes_per_elem, sharded=
             "parallelism": f"dp{world}", "fuse_final": int(fused), "accum_fp32": int(args.accum_fp32),
             "path_bytes_per_elem": path_bytes_per_elem,
             "optimizer": "sharded (SURVEY f2)" if (sharded and world > 1) else "replicated (paper)",
-            "ar_copy_engine": int(getattr(args, "ar_copy_engine", 0)),
+            "ar_copy_engine": int(getattr(args, "ar_copy_engine", 0) or 0), "ar_pieces": int(getattr(args, "ar_pieces", 1) or 1),
             "l2": "inputs (c x 2n B + 16n B state) >> 126 MB L2; no flush"}
 
 
