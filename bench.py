@@ -28,6 +28,9 @@ sys.path.insert(0, ROOT)
 METRIC = "update steps/s & grad elems/s at 1/2/4/8 B200; HBM GB/s and bus GB/s vs peak"
 UNIT = "grad elems/s"
 NVLINK_NOMINAL_GBS = 900.0
+# measured NVLink roofline of the all-reduce's traffic shape on this pool: SM 256-bit loads from and stores to a peer
+# at once, per direction (tools/nvlink_probe.cu "pullpush", best shape, 4 x B200: profiles/r2/j_w4/nvlink_probe.jsonl)
+NVLINK_MEASURED_GBS = 675.0
 
 
 def parse():
@@ -722,7 +725,8 @@ def bus_gbs(stats, steps, n, world, sharded):
     phases = 1 if sharded else 2
     bus = phases * n * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9
     return {"ms_per_step": ar_ms, "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS,
-            "frac_of_770_measured_peer": bus / 770.0, "in_situ": "concurrent with K1 / Adam"}
+            "frac_of_measured_nvlink": bus / NVLINK_MEASURED_GBS, "measured_nvlink_gbs": NVLINK_MEASURED_GBS,
+            "in_situ": "concurrent with K1 / Adam"}
 
 
 def bind_to_gpu_numa(local):

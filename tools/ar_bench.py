@@ -58,7 +58,7 @@ def main():
         for name, ms, nb in out:
             bus = 2 * n * 2 * (world - 1) / world / (ms * 1e-3) / 1e9
             print(json.dumps({"world": world, "impl": name, "buckets": nb, "bytes": 2 * n, "ms": ms,
-                              "bus_gbs": bus, "frac_of_900": bus / 900, "frac_of_770_measured_peer": bus / 770}))
+                              "bus_gbs": bus, "frac_of_900": bus / 900, "frac_of_measured_nvlink_675": bus / 675}))
     dist.destroy_process_group()
 
 
