@@ -91,6 +91,20 @@ def main():
     for split in (1, 2, 4):
         report(f"push all-to-all W={n}", allpairs, split)
 
+    # rotating partners, one stream per GPU: in round j GPU a sends to a + 1 + j (a perfect matching per round)
+    def rotate(starts):
+        for a in devs:
+            st = streams[a][0]
+            st.wait_event(starts[a])
+            with torch.cuda.stream(st):
+                for j in range(n - 1):
+                    b = (a + 1 + j) % n
+                    dst[b][a].copy_(src[a], non_blocking=True)
+            torch.cuda.current_stream(a).wait_stream(st)
+    ms = timed(rotate, devs)
+    print(json.dumps({"probe": f"push rotating partners W={n}", "mib": MB, "ms": ms,
+                      "out_gbs_per_gpu": (n - 1) * nbytes / (ms * 1e-3) / 1e9}), flush=True)
+
     # the same all-to-all push while an HBM-bound copy runs on every GPU (the in-situ question)
     big = {d: torch.empty(1 << 30, dtype=torch.uint8, device=d) for d in devs}
     big2 = {d: torch.empty(1 << 30, dtype=torch.uint8, device=d) for d in devs}
