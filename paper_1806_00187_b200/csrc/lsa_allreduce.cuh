@@ -6,8 +6,9 @@
 //
 //   LsaPeers    W processes, one GPU each (the product at world > 1).  The accumulator is one NCCL symmetric window
 //               (ncclMemAlloc + ncclCommWindowRegister), so every rank's accumulator is load/store-accessible from
-//               every GPU of the NVLink domain ("LSA" peers, NCCL device API); ranks meet at NCCL LSA barriers
-//               inside the kernel.  One launch per rank.
+//               every GPU of the NVLink domain ("LSA" peers, NCCL device API); ranks meet inside the kernel, at
+//               a grid-level flag barrier (bucket kernels, FlagBar) or an NCCL LSA barrier (1-CTA kernels).  One
+//               launch per rank.
 //   LocalPeers  W virtual ranks held as W windows (plain cudaMalloc) on ONE GPU (smpu_group_init): the same kernel
 //               bodies, with rank p's window at base[p].  A single launch covers every rank -- CTAs
 //               [r*per_rank, (r+1)*per_rank) act for rank r -- and the ranks meet at kernel boundaries instead of

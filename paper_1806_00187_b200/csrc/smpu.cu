@@ -1461,7 +1461,8 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
                "ncclCommWindowRegister");
             ncclDevCommRequirements reqs;
             memset(&reqs, 0, sizeof reqs);
-            // one per all-reduce CTA + early decision + late decision + end-of-update (sharded)
+            // indices 0 / 1: the copy-engine all-reduce's barrier kernels; grid_ar .. grid_ar + 2: early decision,
+            // late decision, end of update (sharded).  The bucket kernels meet through their own flag barrier.
             reqs.lsaBarrierCount = ctx->grid_ar + 3;
             reqs.lsaMultimem = cfg->ar_mcast != 0;
             ncclResult_t r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
