@@ -109,9 +109,9 @@ struct LsaPeers {
     // exit: the launch's last CTA advances q and, with `cross`, waits until every rank's CTAs have stored
     // everything (their peer stores included); the other CTAs leave at once.
     __device__ __forceinline__ void leave(int W, unsigned long long q, bool cross) const {
-        __threadfence_system();
-        __syncthreads();
+        __syncthreads();   // the CTA's stores happen before thread 0's system fence (cumulativity)
         if (threadIdx.x == 0) {
+            __threadfence_system();
             const unsigned old = atomicAdd((unsigned*)&fb.ctl[2], 1u);
             if (old == gridDim.x - 1) {
                 __threadfence_system();
