@@ -6,9 +6,8 @@
 //
 //   LsaPeers    W processes, one GPU each (the product at world > 1).  The accumulator is one NCCL symmetric window
 //               (ncclMemAlloc + ncclCommWindowRegister), so every rank's accumulator is load/store-accessible from
-//               every GPU of the NVLink domain ("LSA" peers, NCCL device API); ranks meet inside the kernel, at
-//               a grid-level flag barrier (bucket kernels, FlagBar) or an NCCL LSA barrier (1-CTA kernels).  One
-//               launch per rank.
+//               every GPU of the NVLink domain ("LSA" peers, NCCL device API); ranks meet at NCCL LSA barriers
+//               inside the kernel.  One launch per rank.
 //   LocalPeers  W virtual ranks held as W windows (plain cudaMalloc) on ONE GPU (smpu_group_init): the same kernel
 //               bodies, with rank p's window at base[p].  A single launch covers every rank -- CTAs
 //               [r*per_rank, (r+1)*per_rank) act for rank r -- and the ranks meet at kernel boundaries instead of
@@ -34,38 +33,9 @@ namespace smpu {
 constexpr int kMaxLsaRanks = 8;
 
 // ------------------------------------------------------------------------------------------------ peer policies
-// Grid-level cross-rank barrier of the bucket kernels (k_ar16 / k_ar32 / k_rs): one NVLink exchange per launch
-// instead of one NCCL LSA barrier per CTA.  Each rank owns W 64-bit arrival slots at window offset `slot_off`; in
-// launch number q (identical sequence on every rank) the entry phase publishes 2q + 1 and the exit phase 2q + 2
-// into slot `me` of every rank's window, and waits until all W of its own slots reach the target.  ctl[0] = q (read
-// by every CTA at entry, advanced by the launch's last CTA), ctl[1] = "go" (CTA 0 -> the other CTAs of this rank),
-// ctl[2] = CTAs done (reset by the last one).
-struct FlagBar {
-    size_t slot_off = 0;
-    unsigned long long* ctl = nullptr;
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 struct LsaPeers {
     ncclDevComm dc;
     ncclWindow_t win;
-    FlagBar fb;
     __device__ __forceinline__ int rank() const { return dc.lsaRank; }
     __device__ __forceinline__ int cta() const { return (int)blockIdx.x; }
     __device__ __forceinline__ int ctas() const { return (int)gridDim.x; }
@@ -78,50 +48,6 @@ struct LsaPeers {
         ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), idx);
         bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
     }
-    // thread 0 only: publish `target` in slot `me` of every rank's window, wait for all W of mine
-    __device__ __forceinline__ void exchange(int W, unsigned long long target) const {
-        const int me = rank();
-        __threadfence_system();
-        for (int p = 0; p < W; ++p) st_release_sys((unsigned long long*)at(p, fb.slot_off) + me, target);
-        const unsigned long long* mine = (const unsigned long long*)at(me, fb.slot_off);
-        for (int p = 0; p < W; ++p)
-            while (ld_acquire_sys(mine + p) < target) {
-            }
-    }
-    // entry of a bucket kernel: every rank has launched it, so every rank's earlier stream work (the bucket's
-    // last K1) is complete and visible.  Returns the launch number q (same in every CTA).
-    __device__ __forceinline__ unsigned long long enter(int W) const {
-        __shared__ unsigned long long s_q;
-        if (threadIdx.x == 0) {
-            const unsigned long long q = *(volatile unsigned long long*)&fb.ctl[0];
-            if (blockIdx.x == 0) {
-                exchange(W, 2 * q + 1);
-                st_release_gpu(&fb.ctl[1], 2 * q + 1);
-            } else {
-                while (ld_acquire_gpu(&fb.ctl[1]) < 2 * q + 1) {
-                }
-            }
-            s_q = q;
-        }
-        __syncthreads();
-        return s_q;
-    }
-    // exit: the launch's last CTA advances q and, with `cross`, waits until every rank's CTAs have stored
-    // everything (their peer stores included); the other CTAs leave at once.
-    __device__ __forceinline__ void leave(int W, unsigned long long q, bool cross) const {
-        __syncthreads();   // the CTA's stores happen before thread 0's system fence (cumulativity)
-        if (threadIdx.x == 0) {
-            __threadfence_system();
-            const unsigned old = atomicAdd((unsigned*)&fb.ctl[2], 1u);
-            if (old == gridDim.x - 1) {
-                __threadfence_system();
-                *(volatile unsigned*)&fb.ctl[2] = 0;
-                if (cross) exchange(W, 2 * q + 2);
-                *(volatile unsigned long long*)&fb.ctl[0] = q + 1;
-                __threadfence();
-            }
-        }
-    }
 };
 
 struct LocalPeers {
@@ -133,8 +59,6 @@ struct LocalPeers {
     __device__ __forceinline__ int ctas() const { return per_rank ? per_rank : (int)gridDim.x; }
     __device__ __forceinline__ char* at(int p, size_t off) const { return base[p] + off; }
     __device__ __forceinline__ void sync(uint32_t) const {}   // the launch boundary is the barrier
-    __device__ __forceinline__ unsigned long long enter(int) const { return 0; }
-    __device__ __forceinline__ void leave(int, unsigned long long, bool) const {}
 };
 
 // ------------------------------------------------------------------------------------------------ peer accesses
@@ -202,7 +126,7 @@ __device__ __forceinline__ void head_tail(uint16_t* const* base, int64_t lo, int
 // 16-byte units (smpu_config.ar_vec_bytes = 16), two per thread in flight.
 template <int W, class Peers>
 __global__ void __launch_bounds__(256) k_ar16(Peers pe, int64_t lo, int64_t hi) {
-    const unsigned long long q = pe.enter(W);   // every rank's last K1 of this bucket is complete and visible
+    pe.sync(pe.cta());   // every rank's last K1 of this bucket is complete and visible
     uint16_t* base[W];
 #pragma unroll
     for (int p = 0; p < W; ++p) base[p] = (uint16_t*)pe.at(p, 0);
@@ -251,7 +175,7 @@ __global__ void __launch_bounds__(256) k_ar16(Peers pe, int64_t lo, int64_t hi) 
         for (int p = 0; p < W; ++p) st128_peer(base[p] + i0, a[0]);
     }
     if (me == 0) head_tail<W, true>(base, lo, hi, v0, v1, tid, nthr);
-    pe.leave(W, q, true);   // every shard of every rank has been written
+    pe.sync(pe.cta());   // every shard of every rank has been written
 }
 
 // 32-byte units (256-bit peer loads/stores, the default), U units per thread per iteration: fewer, wider NVLink
@@ -260,7 +184,7 @@ __global__ void __launch_bounds__(256) k_ar16(Peers pe, int64_t lo, int64_t hi) 
 // computed once, by the shard's owner, in ascending rank order, as before).
 template <int W, class Peers, bool MC = false, int U = 1>
 __global__ void __launch_bounds__(512) k_ar32(Peers pe, int64_t lo, int64_t hi) {
-    const unsigned long long q = pe.enter(W);
+    pe.sync(pe.cta());
     uint16_t* base[W];
 #pragma unroll
     for (int p = 0; p < W; ++p) base[p] = (uint16_t*)pe.at(p, 0);
@@ -300,7 +224,7 @@ __global__ void __launch_bounds__(512) k_ar32(Peers pe, int64_t lo, int64_t hi) 
         }
     }
     if (me == 0) head_tail<W, true>(base, lo, hi, v0, v1, tid, nthr);
-    pe.leave(W, q, true);
+    pe.sync(pe.cta());
 }
 
 // ------------------------------------------------------------------- copy-engine variant (smpu_config.ar_copy_engine)
@@ -457,7 +381,7 @@ __global__ void k0_late_x(Peers pe, size_t area_off, DecArgsW A, int ring_mask, 
 // the end-of-update barrier orders every rank's reads of my accumulator before anybody's next update overwrites it.
 template <int W, class Peers>
 __global__ void __launch_bounds__(256) k_rs(Peers pe, int64_t lo, int64_t hi) {
-    const unsigned long long q = pe.enter(W);
+    pe.sync(pe.cta());
     uint16_t* base[W];
 #pragma unroll
     for (int p = 0; p < W; ++p) base[p] = (uint16_t*)pe.at(p, 0);
@@ -482,7 +406,6 @@ __global__ void __launch_bounds__(256) k_rs(Peers pe, int64_t lo, int64_t hi) {
         st128_peer(base[me] + i0, a[0]);
     }
     if (me == 0) head_tail<W, false>(base, lo, hi, v0, v1, tid, nthr);
-    pe.leave(W, q, false);
 }
 
 // Adam on [lo, hi) of my shard (one-shot), w16 stored into every rank's window at window offset w16_off.

@@ -39,9 +39,6 @@ namespace {
 thread_local std::string g_err;
 constexpr int kRing = 64;
 constexpr int64_t kStageElems = int64_t(16) << 20;   // 32 MiB of fp16 per host-staging buffer
-// decision area of the window: early-exchange slots (2 parities x 8 ranks x 16 B) at 0, late ones at 256, the
-// bucket kernels' arrival slots (8 x 8 B, FlagBar) here
-constexpr size_t kBarSlotsOff = 1024;
 
 smpu_status set_err(smpu_status s, const char* fmt, ...) {
     char buf[512];
@@ -99,7 +96,6 @@ struct smpu_ctx {
     int ar_unroll = 1, ar_threads = 256;                    // fused all-reduce shape (smpu_config.ar_*)
     // copy-engine all-reduce (smpu_config.ar_copy_engine): staging offset in the window of every piece, every rank's
     // window as a VA of this process (LSA peers; the copies' destinations), W - 1 copy streams and their events
-    unsigned long long* bar_ctl = nullptr;                   // the bucket kernels' grid barrier state (FlagBar)
     bool ce = false;
     std::vector<std::vector<size_t>> ce_off;
     char* peer_win[kMaxLsaRanks] = {};
@@ -352,12 +348,7 @@ smpu_status launch_k1(smpu_ctx* ctx, const uint16_t* g, int64_t lo, int64_t hi, 
     return SMPU_OK;
 }
 
-LsaPeers lsa_peers(const smpu_ctx* ctx) {
-    LsaPeers pe{ctx->devcomm, ctx->win};
-    pe.fb.slot_off = ctx->dec_area_off + kBarSlotsOff;
-    pe.fb.ctl = ctx->bar_ctl;
-    return pe;
-}
+LsaPeers lsa_peers(const smpu_ctx* ctx) { return LsaPeers{ctx->devcomm, ctx->win}; }
 
 // rank p's window = member p's window allocation; per_rank > 0: one launch for every rank, else one for `fixed`
 LocalPeers local_peers(const smpu_group* g, int per_rank, int fixed) {
@@ -1057,7 +1048,6 @@ void free_ctx(smpu_ctx* c) {
     if (c->acc_from_nccl) ncclMemFree(c->acc);
     else cudaFree(c->acc);
     cudaFree(c->flag);
-    cudaFree(c->bar_ctl);
     cudaFree(c->stat);
     cudaFree(c->xs);
     cudaFree(c->st);
@@ -1338,8 +1328,6 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
     }
     if (ctx->w16_in_win) ctx->w16 = (uint16_t*)((char*)ctx->acc + ctx->w16_off);
     else IK(cudaMalloc(&ctx->w16, n * 2));
-    IK(cudaMalloc(&ctx->bar_ctl, 64));
-    IK(cudaMemset(ctx->bar_ctl, 0, 64));
     IK(cudaMalloc(&ctx->flag, sizeof(int)));
     IK(cudaMalloc(&ctx->stat, sizeof(uint32_t)));
     IK(cudaMalloc(&ctx->tok_dev, sizeof(int64_t)));
@@ -1461,8 +1449,8 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
                "ncclCommWindowRegister");
             ncclDevCommRequirements reqs;
             memset(&reqs, 0, sizeof reqs);
-            // indices 0 / 1: the copy-engine all-reduce's barrier kernels; grid_ar .. grid_ar + 2: early decision,
-            // late decision, end of update (sharded).  The bucket kernels meet through their own flag barrier.
+            // one per all-reduce CTA (indices 0 / 1 also serve the copy-engine all-reduce's barrier kernels) +
+            // early decision + late decision + end-of-update (sharded)
             reqs.lsaBarrierCount = ctx->grid_ar + 3;
             reqs.lsaMultimem = cfg->ar_mcast != 0;
             ncclResult_t r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
