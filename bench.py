@@ -619,6 +619,9 @@ def own_launches(stats, ar_impl, nccl_impl):
     return int(sum(v["launches"] for k, v in stats.items() if k not in lib_kinds))
 
 
+_TRACE_N = [0]
+
+
 def measure(args, step, grads, toks, stream, world, local, resident=True):
     """Time one ctx: a call-by-call region (kernel events -> per-kernel table, roofline) and the captured CUDA graph of
     the same update (the headline unless --no-graph), each after warm-up and a ~0.6 s soak under the clock sampler,
@@ -656,7 +659,9 @@ def measure(args, step, grads, toks, stream, world, local, resident=True):
     out = {"ms_calls": ev0.elapsed_time(ev1) / args.steps, "clk": clk}
     out["ms"] = out["ms_calls"]
     if args.trace:
-        with open(args.trace if world == 1 else f"{args.trace}.rank{step.rank}", "w") as f:
+        # one file per timed ctx of the run (headline, sharded variant, world = 1 baseline ...), per rank
+        _TRACE_N[0] += 1
+        with open(f"{args.trace}.{_TRACE_N[0]}" + ("" if world == 1 else f".rank{step.rank}"), "w") as f:
             for kname, sname, a, b in step.kernel_trace():
                 f.write(json.dumps({"rank": step.rank, "kernel": kname, "stream": sname, "start_ms": round(a, 4),
                                     "end_ms": round(b, 4)}) + "\n")
