@@ -54,6 +54,8 @@ def parse():
                          "each followed by its Adam; default 2 (measured best or equal at W = 2 / 4, c = 16 / 1: "
                          "profiles/r2/f_w4/c4_w4_pieces.jsonl)")
     ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
+    ap.add_argument("--ar-unroll", type=int, choices=[1, 2], default=1, help="smpu_config.ar_unroll")
+    ap.add_argument("--ar-threads", type=int, choices=[256, 512], default=256, help="smpu_config.ar_threads")
     ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1, 2], default=None,
                     help="smpu_config.ar_copy_engine (replicated, W > 1): the bucket all-reduce's NVLink traffic by "
                          "the copy engines (cudaMemcpyAsync push + all-gather, SM fold only); 2: all buckets but the "
@@ -797,7 +799,7 @@ def main_ours(args):
     def make_cfg(sharded, fuse_final=args.fuse_final):
         cfg = P.config_default(update_freq=c, bucket_bytes=int(args.bucket_mib * (1 << 20)), allreduce=ar,
                                sharded=int(sharded), fuse_final=fuse_final, accum_fp32=int(args.accum_fp32),
-                               ar_ctas=args.ar_ctas)
+                               ar_ctas=args.ar_ctas, ar_unroll=args.ar_unroll, ar_threads=args.ar_threads)
         if args.ar_pieces is not None:
             cfg.ar_pieces = args.ar_pieces
         if not sharded:

@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--pieces", default="1", help="comma list of smpu_config.ar_pieces values to time")
     ap.add_argument("--ce", default="0", help="comma list of smpu_config.ar_copy_engine values to time")
+    ap.add_argument("--shape", default="148x256x1",
+                    help="comma list of all-reduce shapes CTAS x THREADS x UNROLL (smpu_config.ar_ctas/threads/unroll)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -112,10 +114,13 @@ def main():
         s1 = P.UpdateStep(wl.numel, theta0, base_cfg, world=1, rank=0, device=local)
         t1 = mx(graph_ms(s1, grads, toks, 1))
         s1.close()
-        for mib, split, ce in [(float(x), int(y), int(z)) for x in args.mib.split(",") for y in args.pieces.split(",")
-                               for z in args.ce.split(",")]:
+        for mib, split, ce, shape in [(float(x), int(y), int(z), sh) for x in args.mib.split(",")
+                                      for y in args.pieces.split(",") for z in args.ce.split(",")
+                                      for sh in args.shape.split(",")]:
+            ctas, threads, unroll = (int(v) for v in shape.split("x"))
             cfg = P.config_default(update_freq=c, bucket_bytes=int(mib * (1 << 20)), sharded=int(args.sharded),
-                                   ar_pieces=split, ar_copy_engine=ce)
+                                   ar_pieces=split, ar_copy_engine=ce, ar_ctas=ctas, ar_threads=threads,
+                                   ar_unroll=unroll)
             cfg.growth_interval = 1 << 40
             t0 = time.perf_counter()
             st = P.UpdateStep(wl.numel, theta0, cfg, world=world, rank=rank, nccl_id=new_id(), device=local)
@@ -127,7 +132,7 @@ def main():
             assert res["applied"] == 1, res
             phases = 1 if args.sharded else 2
             bus = phases * n * 2 * (world - 1) / world / (cm * 1e-3) / 1e9 if cm > 0 else None
-            row = {"world": world, "update_freq": c, "bucket_mib": mib, "ar_pieces": split, "ar_copy_engine": ce,
+            row = {"world": world, "update_freq": c, "bucket_mib": mib, "ar_pieces": split, "ar_copy_engine": ce, "ar_shape": shape,
                    "n_buckets": st.n_buckets,
                    "layout": "sharded" if args.sharded else "replicated", "T_update_ms": T, "T_world1_ms": t1,
                    "exposed_ms": T - t1, "exposed_frac_of_update": (T - t1) / T, "comm_ms": cm,
