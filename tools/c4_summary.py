@@ -21,13 +21,14 @@ def main():
              ""]
     for w, c in keys:
         lines.append(f"## W = {w}, update_freq = {c}")
-        lines.append(f"{'MiB':>6} {'pieces':>6} {'ce':>3} {'buckets':>7} {'T_ms':>7} {'T1_ms':>7} {'exposed_ms':>10} "
+        lines.append(f"{'MiB':>6} {'pieces':>6} {'ce':>3} {'shape':>10} {'buckets':>7} {'T_ms':>7} {'T1_ms':>7} {'exposed_ms':>10} "
                      f"{'exp/T':>6} {'comm_ms':>8} {'exp/comm':>8} {'bus_GB/s':>8}  file")
         sel = [d for d in rows if d["world"] == w and d["update_freq"] == c]
-        sel.sort(key=lambda d: (d["bucket_mib"], d.get("ar_pieces", 1), d.get("ar_copy_engine", 0)))
+        sel.sort(key=lambda d: (d["bucket_mib"], d.get("ar_pieces", 1), d.get("ar_copy_engine", 0),
+                                d.get("ar_shape", "")))
         for d in sel:
             lines.append(f"{d['bucket_mib']:>6.0f} {d.get('ar_pieces', d.get('ar_tail_split', 1)):>6} "
-                         f"{d.get('ar_copy_engine', 0):>3} {d['n_buckets']:>7} {d['T_update_ms']:>7.3f} "
+                         f"{d.get('ar_copy_engine', 0):>3} {d.get('ar_shape', '148x256x1'):>10} {d['n_buckets']:>7} {d['T_update_ms']:>7.3f} "
                          f"{d['T_world1_ms']:>7.3f} {d['exposed_ms']:>10.3f} {d['exposed_frac_of_update']:>6.1%} "
                          f"{d['comm_ms']:>8.3f} {d['exposed_frac_of_comm']:>8.1%} {d['bus_gbs_in_situ']:>8.0f}  "
                          f"{d['_file']}")
