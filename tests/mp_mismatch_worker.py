@@ -23,7 +23,8 @@ def main():
     theta0 = np.zeros(sum(numel), np.float32)
     fails = []
     cases = [dict(ar_ctas=64 + rank), dict(ar_threads=256 if rank == 0 else 512), dict(update_freq=2 + rank),
-             dict(bucket_bytes=(1 << 20) + rank), dict(sharded=rank % 2)]
+             dict(bucket_bytes=(1 << 20) + rank), dict(sharded=rank % 2), dict(ar_copy_engine=rank % 2),
+             dict(ar_pieces=1 + rank)]
     for kw in cases:
         obj = [P.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -37,8 +38,8 @@ def main():
                 fails.append(f"{kw}: rank {rank} got {ex}")
     obj = [P.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    st = P.UpdateStep(numel, theta0, P.config_default(update_freq=1, ar_ctas=32), world=world, rank=rank,
-                      nccl_id=obj[0], device=local)
+    st = P.UpdateStep(numel, theta0, P.config_default(update_freq=1, ar_ctas=32, ar_copy_engine=1), world=world,
+                      rank=rank, nccl_id=obj[0], device=local)
     g = torch.ones(sum(numel), dtype=torch.float16, device="cuda").view(torch.int16)
     st.accumulate(g, 10)
     r = st.step()

@@ -75,8 +75,8 @@ def _run(world, family="real", sharded=False, mode="calls", updates=6, **cfg_kw)
     wl = _workload(world, family, updates)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
-    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, bucket_bytes=400_000, sharded=int(sharded), **cfg_kw),
-                         world=world)
+    cfg_kw.setdefault("bucket_bytes", 400_000)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, sharded=int(sharded), **cfg_kw), world=world)
     members = grp.members
     bb = members[0].bucket_begin
     assert len(bb) - 1 >= 2 and any(int(x) % 16 for x in bb[1:-1]), "buckets must cut off the vector grid"
@@ -167,6 +167,14 @@ def test_virtual_copy_engine(world, mode, split, ce):
     ascending-rank order), alone and with ar_pieces, through every injection kind; ce = 2: every bucket but the last
     on the copy engines, the last through k_ar32 (the two share the LSA barriers)."""
     _run(world, "real", False, mode=mode, ar_copy_engine=ce, ar_pieces=split)
+
+
+@pytest.mark.parametrize("world,ce,sharded", [(3, 0, False), (8, 1, False), (5, 2, False), (6, 0, True)])
+def test_virtual_one_bucket_per_tensor(world, ce, sharded):
+    """bucket_bytes = 2: every tensor its own bucket, down to the 7-element bias -- buckets with no whole 16-element
+    unit (the fold is all head / tail, the copy engines move nothing), shards empty on most ranks; SM, copy-engine
+    and copy-engine-but-last all-reduces and the sharded layout, bitwise against the oracle."""
+    _run(world, "real", sharded, mode="calls", bucket_bytes=2, ar_copy_engine=ce)
 
 
 @pytest.mark.parametrize("world,sharded", [(4, False), (7, True)])
