@@ -57,6 +57,22 @@ int smpu_sched_time_balanced(const int32_t* src_len, const int32_t* tgt_len, int
 int smpu_sched_simulate(const double* batch_seconds, int64_t n_batches, int workers, int update_freq,
                         double* wall, double* idle_fraction, int64_t* steps);
 
+/* The paper's overlap of the bucketed all-reduce with the backward ("we add the result to a
+ * synchronization buffer.  As soon as the size of the buffer reaches a predefined threshold we synchronize the
+ * buffered gradients in a background thread"), as SPEC's analytic schedule: layers arrive in backward
+ * (reverse) order, layer i ready at the sum of backward_seconds[0..i]; the buffer is flushed once it holds
+ * >= threshold_bytes (threshold 0: every layer) and whatever is left at the end of the backward; flushes run FIFO on
+ * one channel, a flush of b bytes costing latency + b / bytes_per_second x 2 (W-1) / W (W = workers;
+ * W = 1 costs nothing).  Per flush k: the last layer in it, ready time, start and end on the channel (arrays of
+ * cap_buckets, may be NULL).  *total_overlap = the later of the backward's end and the last flush's end;
+ * *total_serial = the backward + one flush of all bytes after it.  Returns 2 if more than cap_buckets flushes
+ * (*n_buckets then tells how many). */
+int smpu_sched_overlap_schedule(const double* layer_bytes, const double* backward_seconds, int64_t n_layers,
+                                double threshold_bytes, double latency_seconds, double bytes_per_second, int workers,
+                                int64_t* bucket_last_layer, double* bucket_ready, double* bucket_start,
+                                double* bucket_end, int64_t cap_buckets, int64_t* n_buckets, double* total_overlap,
+                                double* total_serial);
+
 #ifdef __cplusplus
 }
 #endif

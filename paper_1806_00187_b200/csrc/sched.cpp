@@ -196,4 +196,49 @@ int smpu_sched_simulate(const double* batch_seconds, int64_t n_batches, int work
     return 0;
 }
 
+int smpu_sched_overlap_schedule(const double* layer_bytes, const double* backward_seconds, int64_t n_layers,
+                                double threshold_bytes, double latency_seconds, double bytes_per_second, int workers,
+                                int64_t* bucket_last_layer, double* bucket_ready, double* bucket_start,
+                                double* bucket_end, int64_t cap_buckets, int64_t* n_buckets, double* total_overlap,
+                                double* total_serial) {
+    if (n_layers < 0 || (n_layers > 0 && (!layer_bytes || !backward_seconds)) || !(threshold_bytes >= 0) ||
+        !(latency_seconds >= 0) || !(bytes_per_second > 0) || workers < 1 || !n_buckets || !total_overlap ||
+        !total_serial || cap_buckets < 0)
+        return 1;
+    for (int64_t i = 0; i < n_layers; ++i)
+        if (!(layer_bytes[i] >= 0) || !(backward_seconds[i] >= 0)) return 1;
+    // ring all-reduce cost of b bytes over `workers`; a flush of nothing costs nothing
+    const double ring = workers > 1 ? 2.0 * (workers - 1) / workers : 0.0;
+    auto cost = [&](double b) { return b > 0 ? latency_seconds + b / bytes_per_second * ring : 0.0; };
+    int64_t nb = 0;
+    double t = 0, buffered = 0, channel_free = 0, total_bytes = 0, backward = 0;
+    bool pending = false;
+    auto flush = [&](int64_t last_layer) {
+        const double start = std::max(t, channel_free), end = start + cost(buffered);
+        if (nb < cap_buckets) {
+            if (bucket_last_layer) bucket_last_layer[nb] = last_layer;
+            if (bucket_ready) bucket_ready[nb] = t;
+            if (bucket_start) bucket_start[nb] = start;
+            if (bucket_end) bucket_end[nb] = end;
+        }
+        channel_free = end;
+        buffered = 0;
+        pending = false;
+        ++nb;
+    };
+    for (int64_t i = 0; i < n_layers; ++i) {
+        t += backward_seconds[i];            // layer i's gradient is ready
+        backward += backward_seconds[i];
+        buffered += layer_bytes[i];
+        total_bytes += layer_bytes[i];
+        pending = true;
+        if (buffered >= threshold_bytes) flush(i);   // threshold 0: every layer
+    }
+    if (pending) flush(n_layers - 1);        // the rest at the end of the backward
+    *n_buckets = nb;
+    *total_overlap = std::max(backward, channel_free);
+    *total_serial = backward + cost(total_bytes);
+    return nb > cap_buckets ? 2 : 0;
+}
+
 }  // extern "C"

@@ -25,8 +25,10 @@ def lib():
         L.smpu_sched_time_balanced.argtypes = [p, p, i64, p, d, p, p, i64, P(ctypes.c_int64)]
         L.smpu_sched_simulate.argtypes = [p, i64, i32, i32, P(ctypes.c_double), P(ctypes.c_double),
                                           P(ctypes.c_int64)]
+        L.smpu_sched_overlap_schedule.argtypes = [p, p, i64, d, d, d, i32, p, p, p, p, i64, P(ctypes.c_int64),
+                                                  P(ctypes.c_double), P(ctypes.c_double)]
         for f in ("smpu_sched_token_budget", "smpu_sched_fit_timing", "smpu_sched_estimate",
-                  "smpu_sched_time_balanced", "smpu_sched_simulate"):
+                  "smpu_sched_time_balanced", "smpu_sched_simulate", "smpu_sched_overlap_schedule"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -96,3 +98,21 @@ def simulate(batch_seconds, workers, update_freq):
     _check(lib().smpu_sched_simulate(_p(t), t.size, workers, update_freq, ctypes.byref(wall), ctypes.byref(idle),
                                      ctypes.byref(steps)), "simulate")
     return dict(wall=wall.value, idle_fraction=idle.value, steps=steps.value)
+
+
+def overlap_schedule(layer_bytes, backward_seconds, threshold_bytes, latency_seconds, bytes_per_second, workers):
+    """SPEC S:405-413 (include/smpu_sched.h): -> dict(buckets=[(last_layer, ready, start, end)], total_overlap,
+    total_serial)."""
+    b = np.ascontiguousarray(layer_bytes, dtype=np.float64)
+    t = np.ascontiguousarray(backward_seconds, dtype=np.float64)
+    cap = max(b.size, 1)
+    last = np.zeros(cap, np.int64)
+    ready, start, end = (np.zeros(cap, np.float64) for _ in range(3))
+    nb, tov, tser = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+    _check(lib().smpu_sched_overlap_schedule(_p(b), _p(t), b.size, float(threshold_bytes), float(latency_seconds),
+                                             float(bytes_per_second), int(workers), _p(last), _p(ready), _p(start),
+                                             _p(end), cap, ctypes.byref(nb), ctypes.byref(tov), ctypes.byref(tser)),
+           "overlap_schedule")
+    k = nb.value
+    return dict(buckets=[(int(last[i]), ready[i], start[i], end[i]) for i in range(k)], total_overlap=tov.value,
+                total_serial=tser.value)

@@ -111,3 +111,71 @@ def test_simulator(S):
     idle = [S.simulate(t, 8, c)["idle_fraction"] for c in (1, 2, 4, 8, 16)]
     assert idle[-1] < idle[0]                                                       # S:422 / P:179, Fig. 2
     assert all(a >= b - 1e-3 for a, b in zip(idle, idle[1:]))                      # S:440 (statistical)
+
+
+# ---- the analytic overlap schedule
+def test_overlap_degenerate_threshold_is_serial(S):
+    """threshold > total bytes -> one flush at the end; overlap time = serial time."""
+    b, t = [3e6, 5e6, 2e6], [0.01, 0.02, 0.005]
+    r = S.overlap_schedule(b, t, 1e9, 1e-4, 1e9, 4)
+    assert len(r["buckets"]) == 1 and r["buckets"][0][0] == 2
+    assert r["total_overlap"] == pytest.approx(r["total_serial"], rel=1e-12)
+    assert r["total_serial"] == pytest.approx(0.035 + 1e-4 + 10e6 / 1e9 * 1.5, rel=1e-12)
+
+
+def test_overlap_infinitely_fast_comm_hides_entirely(S):
+    """bandwidth -> inf, latency 0 -> overlap time = the backward."""
+    r = S.overlap_schedule([1e6] * 5, [0.1, 0.2, 0.3, 0.4, 0.5], 1.5e6, 0.0, 1e300, 8)
+    assert r["total_overlap"] == pytest.approx(1.5, rel=1e-12)
+
+
+def test_overlap_six_equal_layers_hand_trace(S):
+    """6 equal layers, comm per layer = backward per layer, threshold = 1 layer -> backward + 1 comm slot.
+    Hand-simulated event list: flush k (layer k) ready at k + 1, starts at once, ends at k + 2."""
+    # W = 2: ring factor 2 (W-1)/W = 1, so 1e6 bytes at 1e6 B/s cost 1 s
+    r = S.overlap_schedule([1e6] * 6, [1.0] * 6, 1e6, 0.0, 1e6, 2)
+    assert [(k, rd, st, en) for k, rd, st, en in r["buckets"]] == [(k, k + 1.0, k + 1.0, k + 2.0) for k in range(6)]
+    assert r["total_overlap"] == 7.0 and r["total_serial"] == 12.0
+
+
+def test_overlap_slow_channel_queues_fifo(S):
+    """Comm slower than the backward: flushes queue on the one channel.  Layers ready at 1, 2, 3; each
+    flush costs 0.5 + 1.5 = 2 s -> starts 1, 3, 5, ends 3, 5, 7; serial = 3 + (0.5 + 4.5)."""
+    r = S.overlap_schedule([1.0] * 3, [1.0] * 3, 0.0, 0.5, 1.0, 4)   # W = 4: ring factor 1.5
+    ends = [e for _, _, _, e in r["buckets"]]
+    starts = [s for _, _, s, _ in r["buckets"]]
+    assert starts == pytest.approx([1.0, 3.0, 5.0]) and ends == pytest.approx([3.0, 5.0, 7.0])
+    assert r["total_overlap"] == pytest.approx(7.0) and r["total_serial"] == pytest.approx(3.0 + 0.5 + 4.5)
+
+
+def test_overlap_buckets_partition_layers_and_bound(S):
+    """Random instances: flushes cover the layers in order (each closes at >= threshold, the last takes the rest),
+    the channel never runs two flushes at once, and backward <= overlap <= serial + (flushes - 1) x latency."""
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        n = int(rng.integers(1, 40))
+        b = rng.uniform(0, 5e6, n)
+        t = rng.uniform(0, 2e-3, n)
+        thr = float(rng.uniform(0, 2e7))
+        lat, bw, W = float(rng.uniform(0, 5e-5)), float(rng.uniform(1e10, 1e12)), int(rng.integers(1, 9))
+        r = S.overlap_schedule(b, t, thr, lat, bw, W)
+        lasts = [k for k, *_ in r["buckets"]]
+        assert lasts == sorted(lasts) and lasts[-1] == n - 1
+        lo = 0
+        for k in lasts[:-1]:
+            assert b[lo:k + 1].sum() >= thr and (k == lo or b[lo:k].sum() < thr)
+            lo = k + 1
+        prev_end = 0.0
+        for k, ready, start, end in r["buckets"]:
+            assert ready == pytest.approx(t[:k + 1].sum()) and start >= max(ready, prev_end) - 1e-15
+            prev_end = end
+        assert t.sum() - 1e-12 <= r["total_overlap"] <= r["total_serial"] + len(lasts) * lat + 1e-12
+
+
+def test_overlap_rejects_bad_arguments(S):
+    with pytest.raises(ValueError):
+        S.overlap_schedule([1.0], [1.0], -1.0, 0.0, 1.0, 2)
+    with pytest.raises(ValueError):
+        S.overlap_schedule([1.0], [1.0], 1.0, 0.0, 0.0, 2)
+    with pytest.raises(ValueError):
+        S.overlap_schedule([-1.0], [1.0], 1.0, 0.0, 1.0, 2)
