@@ -29,7 +29,7 @@ BUS = {                 # in-situ bus GB/s of the bucket all-reduce (bench.py al
     ("sm", 2): 566e9, ("sm", 4): 555e9, ("sm", 8): 540e9,      # W = 8: extrapolated (no 8-GPU box in gpurun)
     ("ce", 2): 398e9, ("ce", 4): 330e9, ("ce", 8): 300e9,      # CE: r2/i_ce_w2 c4 (W = 2); W = 4 / 8 estimated
 }
-MEASURED = {            # train c = 1: (ms with overlap, ms without, world = 1 ms) -- profiles/r2/j_w2, r2/j_w4
+MEASURED = {            # train c = 1: (ms with overlap, ms without) -- profiles/r2/j_w2, r2/j_w4
     ("sm", 2): (13.195, 12.976), ("ce", 2): (12.857, 13.031),
     ("sm", 4): (13.452, 13.136), ("ce", 4): (12.857, 13.302),
 }
@@ -63,7 +63,7 @@ def main():
               "Reading: the model charges the exchange no compute and its 'serial' case no overlap at all, so it predicts a",
               "saving for either engine.  Measured, the SM all-reduce's saving is eaten by the SMs it takes from the",
               "backward's GEMMs (a loss), and the library's no-overlap path is not serial either (each bucket's all-reduce",
-              "still overlaps the later buckets' accumulation and Adam), so the copy engines keep a third to a half of the",
+              "still overlaps the later buckets' accumulation and Adam), so the copy engines keep a fifth to a third of the",
               "predicted saving.  The paper's 37 -> 32 min (P:213-214) was InfiniBand between 16 machines, where a flush",
               "costs far more than over NVLink and the predicted saving is the whole story."]
     text = "\n".join(lines)
