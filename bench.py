@@ -689,13 +689,19 @@ def measure(args, step, grads, toks, stream, world, local, resident=True):
         step.kernel_stats(reset=True)
         torch.cuda.synchronize()
         _barrier(world)
+        # an event after every replay on the launch stream: the per-update distribution (SURVEY d.4 p10/p50/p90)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             step.graph_launch(toks, stream)
+            marks[i].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
         _barrier(world)
     out["ms"] = ev0.elapsed_time(ev1) / args.steps
+    per = np.diff([0.0] + [ev0.elapsed_time(m) for m in marks])
+    out["per_update_ms"] = {"p10": float(np.percentile(per, 10)), "p50": float(np.percentile(per, 50)),
+                            "p90": float(np.percentile(per, 90)), "max": float(per.max()), "n": int(per.size)}
     out["gstats"] = step.kernel_stats(reset=True)
     out["clk"] = clk_g
     last = step.result(step.scalars()["attempts"])
@@ -956,6 +962,8 @@ def main_ours(args):
                          "cuda_graph (smpu_graph_launch of the captured update; kernels/roofline from the call path)"}
     if M["graph"]:
         g = dict(M["graph"])
+        if "per_update_ms" in M:
+            g["per_update_ms_rank0"] = M["per_update_ms"]
         g["launches_per_step"] = own_launches(M["gstats"], ar_impl, P.smpu.AR_NCCL) / args.steps
         if ms_res:
             # one pass over the c gradients (+ the accumulator written, then Adam's 28) or, fused, straight into Adam
