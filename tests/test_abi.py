@@ -110,7 +110,7 @@ def test_sched_library_exports_header():
     src = open(os.path.join(ROOT, "include", "smpu_sched.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = sorted(set(re.findall(r"\b(smpu_sched_[a-z_]+)\s*\(", src)))
-    assert len(names) == 5
+    assert len(names) == 6   # token_budget, fit_timing, estimate, time_balanced, simulate, overlap_schedule
     lib = ctypes.CDLL(so)
     for name in names:
         assert hasattr(lib, name), name

@@ -70,13 +70,14 @@ def _feed(members, grads, toks, mode, rng, bb):
         raise ValueError(mode)
 
 
-def _run(world, family="real", sharded=False, mode="calls", updates=6, **cfg_kw):
+def _run(world, family="real", sharded=False, mode="calls", updates=6, acc32=False, **cfg_kw):
     import paper_1806_00187_b200 as P
     wl = _workload(world, family, updates)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
     cfg_kw.setdefault("bucket_bytes", 400_000)
-    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, sharded=int(sharded), **cfg_kw), world=world)
+    ocfg = O.Config(accum_fp32=acc32)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, ocfg, sharded=int(sharded), **cfg_kw), world=world)
     members = grp.members
     bb = members[0].bucket_begin
     assert len(bb) - 1 >= 2 and any(int(x) % 16 for x in bb[1:-1]), "buckets must cut off the vector grid"
@@ -87,7 +88,7 @@ def _run(world, family="real", sharded=False, mode="calls", updates=6, **cfg_kw)
             for lo, hi in rr:
                 mark[lo:hi] += 1
         assert (mark == 1).all(), "shards must partition the vector"
-    orc = O.Oracle(theta0)
+    orc = O.Oracle(theta0, ocfg)
     mags = Magnitudes(theta0)
     rng = np.random.default_rng(world * 131 + len(mode))
     report, seen = [], set()
@@ -175,6 +176,13 @@ def test_virtual_one_bucket_per_tensor(world, ce, sharded):
     unit (the fold is all head / tail, the copy engines move nothing), shards empty on most ranks; SM, copy-engine
     and copy-engine-but-last all-reduces and the sharded layout, bitwise against the oracle."""
     _run(world, "real", sharded, mode="calls", bucket_bytes=2, ar_copy_engine=ce)
+
+
+@pytest.mark.parametrize("world,ce,sharded", [(4, 1, False), (8, 0, False), (3, 0, True)])
+def test_virtual_accum_fp32(world, ce, sharded):
+    """SURVEY Z1's fp32-accumulator knob at W > 1: per-rank binary32 sums, rn16 of the last one, then the same fp16
+    all-reduce (SM or copy engines) and decisions; R bitwise the oracle's binary32 variant (orc_accumulate32)."""
+    _run(world, "real", sharded, mode="buckets", acc32=True, ar_copy_engine=ce)
 
 
 @pytest.mark.parametrize("world,sharded", [(4, False), (7, True)])
