@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) k1_accumulate(uint16_t* __restrict__ acc,
             x = (uint16_t)(s & 0xFFFFu);
         }
         if (DETECT && h_nonfinite(x)) bad |= 1u;
-        if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+        if (STATS) mx = mag_max2(mx, (uint32_t)x);   // per lane: mx holds two packed magnitudes
         acc[i] = x;
     };
     if (vec_ok) {
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256, SMPU_K1_MINB) k1_accumulate_1(uint16_t* _
         uint16_t x = gb[i];
         if (!FIRST) x = (uint16_t)(hadd2_rn((uint32_t)acc[i], (uint32_t)x) & 0xFFFFu);
         if (DETECT && h_nonfinite(x)) bad |= 1u;
-        if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+        if (STATS) mx = mag_max2(mx, (uint32_t)x);   // per lane: mx holds two packed magnitudes
         acc[i] = x;
     };
     if (vec_ok) {
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(256, 4) k1_accumulate_many(uint16_t* __restric
         uint32_t x = FIRST ? (uint32_t)P.g[0][i - lo] : (uint32_t)acc[i];
         for (int k = FIRST ? 1 : 0; k < count; ++k) x = hadd2_rn(x, (uint32_t)P.g[k][i - lo]) & 0xFFFFu;
         if (DETECT && h_nonfinite((uint16_t)x)) bad |= 1u;
-        if (STATS) mx = max(mx, x & 0x7FFFu);
+        if (STATS) mx = mag_max2(mx, (uint32_t)x);   // per lane: mx holds two packed magnitudes
         acc[i] = (uint16_t)x;
     };
     if (vec_ok) {
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) k1_scan(const uint16_t* __restrict__ acc,
     auto elem = [&](int64_t i) {
         uint16_t x = acc[i];
         if (DETECT && h_nonfinite(x)) bad |= 1u;
-        if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+        if (STATS) mx = mag_max2(mx, (uint32_t)x);   // per lane: mx holds two packed magnitudes
     };
     for (int64_t i = lo + tid; i < vbeg; i += nthr) elem(i);
     for (int64_t i = vend + tid; i < hi; i += nthr) elem(i);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(256, SMPU_K1_MINB) k1_acc32(float* __restrict_
         if (OUT16) {
             const uint16_t x = __half_as_ushort(__float2half_rn(a));
             if (DETECT && h_nonfinite(x)) bad |= 1u;
-            if (STATS) mx = max(mx, (uint32_t)(x & 0x7FFFu));
+            if (STATS) mx = mag_max2(mx, (uint32_t)x);   // per lane: mx holds two packed magnitudes
             acc16[i] = x;
         } else {
             A32[i] = a;

@@ -178,6 +178,41 @@ def test_virtual_one_bucket_per_tensor(world, ce, sharded):
     _run(world, "real", sharded, mode="calls", bucket_bytes=2, ar_copy_engine=ce)
 
 
+@pytest.mark.parametrize("world,c,ce,sharded", [(2, 1, 0, False), (3, 2, 1, False), (4, 3, 0, True), (2, 1, 0, True)])
+def test_virtual_nonfinite_in_bucket_head_and_tail(world, c, ce, sharded):
+    """A non-finite in the ragged head or tail of a bucket, handled by a thread that also accumulated a 16-element
+    vector unit: the max |A_r| statistic of the early decision must still see it (regression: the element path once
+    took a scalar max against the two packed lanes of the vector path's max, so an INF at a bucket's first elements
+    was lost and the update applied).  Buckets of one tensor each: [0, 1), [1, 32), [32, 1032), [1032, 1065);
+    INF at 1 (head of bucket 1), NaN at 1031 (tail of bucket 2), -INF at 1064 (tail of the last), each on one rank
+    and micro-batch, then a clean update; decisions and R bitwise the oracle's."""
+    import paper_1806_00187_b200 as P
+    tensors = [("a", 1, 0), ("b", 31, 0), ("c", 1000, 1), ("d", 33, 2)]
+    inj = [dict(u=1, kind="INF", r=0, k=1, i=1), dict(u=2, kind="NAN", r=world - 1, k=c, i=1031),
+           dict(u=3, kind="NINF", r=world // 2, k=1, i=1064)]
+    wl = models.Workload("headtail", tensors, world, c, injections=inj)
+    lay = synth.Layout(wl)
+    theta0 = synth.theta0_cpu(wl, lay)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, bucket_bytes=2, sharded=int(sharded), ar_copy_engine=ce),
+                         world=world)
+    ms = grp.members
+    assert list(ms[0].bucket_begin) == [0, 1, 32, 1032, 1065]
+    orc = O.Oracle(theta0)
+    for u in range(1, 5):
+        grads = [[synth.micro_grad_cpu(wl, lay, u, r, k, orc.e) for k in range(1, c + 1)] for r in range(world)]
+        toks = [[synth.ntokens(wl, u, r, k) for k in range(1, c + 1)] for r in range(world)]
+        for k in range(c):
+            for r in range(world):
+                ms[r].accumulate(h2t(grads[r][k]), toks[r][k])
+        for m in ms:
+            m.step(wait=False)
+        ores = orc.update(grads, toks)
+        assert ores["overflow"] == (u <= 3)
+        for m in ms:
+            assert decisions(m.result(u)) == oracle_decisions(ores), (u, m.rank)
+    grp.close()
+
+
 @pytest.mark.parametrize("world,ce,sharded", [(4, 1, False), (8, 0, False), (3, 0, True)])
 def test_virtual_accum_fp32(world, ce, sharded):
     """SURVEY Z1's fp32-accumulator knob at W > 1: per-rank binary32 sums, rn16 of the last one, then the same fp16
