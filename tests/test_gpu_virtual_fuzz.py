@@ -3,8 +3,9 @@ class), W = 2..8, update_freq 1..4, bucket thresholds from a few bytes to 1 MiB,
 all-reduce (ar_copy_engine 0 / 1 / 2), ar_pieces 1..3, the replicated or sharded layout, every way of interleaving
 the ranks' calls (micro-batch by micro-batch, rank-major, last micro-batch bucket-wise in random rank x bucket order,
 resident accumulate_many), injected non-finites on any rank and micro-batch, RED_OVF (finite everywhere, overflow
-only in the sum) and BIG (a finite 40000 after the sum: the early decision must defer to the sweep); the library vs the oracle (ascending-rank rn16 reduce, reading R3) on decisions and R (bitwise) and
-theta/m/v/w16 (tolerance), every update, replicas identical."""
+only in the sum) and BIG (a finite 40000 after the sum: the early decision must defer to the sweep); the library vs
+the oracle (ascending-rank rn16 reduce, reading R3) on decisions and R (bitwise) and theta/m/v/w16 (tolerance),
+every update, replicas identical."""
 import hashlib
 
 import numpy as np
