@@ -5,7 +5,8 @@ the ranks' calls (micro-batch by micro-batch, rank-major, last micro-batch bucke
 resident accumulate_many), injected non-finites on any rank and micro-batch, RED_OVF (finite everywhere, overflow
 only in the sum) and BIG (a finite 40000 after the sum: the early decision must defer to the sweep); the library vs
 the oracle (ascending-rank rn16 reduce, reading R3) on decisions and R (bitwise) and theta/m/v/w16 (tolerance),
-every update, replicas identical."""
+every update, replicas identical; the fp32 accumulator (Z1) and
+split-tensor buckets in a quarter of the cases each."""
 import hashlib
 
 import numpy as np
@@ -46,26 +47,30 @@ def cases(draw):
     pieces = 1 if sharded else draw(st.integers(1, 3))
     mode = draw(st.sampled_from(["calls", "rank_major", "buckets", "many"]))
     bucket_bytes = draw(st.sampled_from([2, 1000, 16_384, 100_000, 1 << 20]))
-    return tensors, W, c, inj, sharded, ce, pieces, mode, bucket_bytes, draw(st.integers(0, 1000))
+    acc32 = draw(st.integers(0, 3)) == 0          # SURVEY Z1's fp32 accumulator in a quarter of the cases
+    split = draw(st.integers(0, 3)) == 0          # split_tensors: buckets cut through tensors
+    return tensors, W, c, inj, sharded, ce, pieces, mode, bucket_bytes, draw(st.integers(0, 1000)), acc32, split
 
 
 @seed(20261019)
-@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=60, deadline=None, suppress_health_check=list(HealthCheck))
 @given(cases())
 def test_virtual_fuzz_against_oracle(case):
     import paper_1806_00187_b200 as P
-    tensors, W, c, inj, sharded, ce, pieces, mode, bucket_bytes, order_seed = case
+    tensors, W, c, inj, sharded, ce, pieces, mode, bucket_bytes, order_seed, acc32, split = case
     if mode == "many" and c == 1:
         mode = "calls"
     wl = models.Workload("vfuzz", tensors, W, c, injections=inj)
     lay = synth.Layout(wl)
     theta0 = synth.theta0_cpu(wl, lay)
-    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, bucket_bytes=bucket_bytes, sharded=int(sharded),
-                                                   ar_copy_engine=ce, ar_pieces=pieces), world=W)
+    ocfg = O.Config(accum_fp32=acc32)
+    grp = P.VirtualGroup(wl.numel, theta0, lib_cfg(wl, ocfg, bucket_bytes=bucket_bytes, sharded=int(sharded),
+                                                   ar_copy_engine=ce, ar_pieces=pieces, split_tensors=int(split)),
+                         world=W)
     ms = grp.members
     bb = ms[0].bucket_begin
     ranges = [m.shard_ranges() for m in ms]
-    orc = O.Oracle(theta0)
+    orc = O.Oracle(theta0, ocfg)
     mags = Magnitudes(theta0)
     rng = np.random.default_rng(order_seed)
     import tests.test_gpu_virtual as V
