@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2, 1 GPU, at HEAD: the whole -m gpu suite (durations), smoke(), the default N = 1 bench and the reference arm.
 set -x
-O=gpurun_out/r2r
+O=${OUT:-gpurun_out/r2r}
 mkdir -p $O
 cat .head_sha > $O/head.txt
 timeout 2400 python -m pytest tests -m gpu -q -rs --durations=15 > $O/gpu_tests.log 2>&1; echo "pytest rc=$?" >> $O/gpu_tests.log
