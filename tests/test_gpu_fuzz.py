@@ -4,6 +4,8 @@ order / resident accumulate_many / in-place NULL / CUDA graph), fuse_final on or
 (SURVEY Z1 knob) in a quarter of the cases, row-sparse embedding gradients in half, injected non-finites
 anywhere; the library vs the oracle on decisions (bitwise), the accumulator (bitwise, wherever it holds R) and
 theta/m/v/w16 (tolerance), every update."""
+import os
+
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, seed, settings
@@ -45,8 +47,9 @@ def cases(draw):
     return tensors, c, inj, mode, bucket_bytes, order_seed, fuse, acc32, embed_row
 
 
-@seed(20261018)
-@settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck))
+@seed(int(os.environ.get("SMPU_FUZZ_SEED", 20261018)))
+@settings(max_examples=int(os.environ.get("SMPU_FUZZ_EXAMPLES", 150)), deadline=None,
+          suppress_health_check=list(HealthCheck))
 @given(cases())
 def test_fuzz_against_oracle(case):
     import torch

@@ -9,6 +9,8 @@ every update, replicas identical (SURVEY rows a5, a6, f1, 
 split-tensor buckets in a quarter of the cases each; 200 cases (~12 s)."""
 import hashlib
 
+import os
+
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, seed, settings
@@ -52,8 +54,9 @@ def cases(draw):
     return tensors, W, c, inj, sharded, ce, pieces, mode, bucket_bytes, draw(st.integers(0, 1000)), acc32, split
 
 
-@seed(20261019)
-@settings(max_examples=200, deadline=None, suppress_health_check=list(HealthCheck))
+@seed(int(os.environ.get("SMPU_FUZZ_SEED", 20261019)))
+@settings(max_examples=int(os.environ.get("SMPU_FUZZ_EXAMPLES", 200)), deadline=None,
+          suppress_health_check=list(HealthCheck))
 @given(cases())
 def test_virtual_fuzz_against_oracle(case):
     import paper_1806_00187_b200 as P
