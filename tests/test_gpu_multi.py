@@ -45,6 +45,20 @@ def test_copy_engine_allreduce(world, graph, ce):
     _run(world, "real", port=29581 + 2 * world + graph + 8 * (ce - 1), impl="ce" if ce == 1 else "ce2", graph=graph)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_random_cases_on_real_peers(world):
+    """The W > 1 fuzz on real peers (tests/mp_fuzz_worker.py): random layouts, SM / copy-engine / CE-but-last
+    all-reduce, pieces, replicated / sharded, injections; decisions and R bitwise the oracle's, replicas identical."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29601 + world), "tests/mp_fuzz_worker.py",
+           "16" if world == 2 else "10", str(31 + world)]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    print(p.stdout[-3000:], p.stderr[-3000:])
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+
+
 @pytest.mark.parametrize("impl", ["nccl", "fused"])
 def test_world2_cuda_graph(impl):
     """A whole W = 2 update (accumulates, bucket all-reduces, decision exchange, per-bucket Adam) as one graph."""
