@@ -1,4 +1,6 @@
-"""Repro of the virtual fuzz failure: W = 2, c = 1, an INF on rank 0 (u = 1, i = 1), tensors [1, 31]."""
+"""Repro of the first W > 1 fuzz failure (r2t): W = 2, c = 1, an INF on rank 0 (u = 1, i = 1), tensors [1, 31], one
+bucket per tensor -- the update applied although R held the INF (K1's max|A| statistic lost ragged-head values;
+fixed).  Prints decisions, oracle decisions and R[1] for a few layouts."""
 import sys
 import numpy as np
 import torch
