@@ -861,6 +861,28 @@ def main_ours(args):
                "source": "pinned host fp16 micro-gradients, staged H2D inside smpu_accumulate",
                "rank_cpus_numa_local": numa_cpus}
         del host
+    # ---- the bucket all-reduce standalone (SURVEY d.4: "measure it standalone ... and in situ"): the headline ctx's
+    # smpu_allreduce_accumulator back to back, CUDA events, max over ranks (its values are overwritten by the next
+    # update's first K1; nothing else reads them)
+    ar_alone = None
+    if world > 1 and ar_impl == P.smpu.AR_FUSED and not head_sharded:
+        for _ in range(3):
+            step.allreduce_accumulator(stream)
+        torch.cuda.synchronize()
+        _barrier(world)
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        for _ in range(10):
+            step.allreduce_accumulator(stream)
+        b_ev.record(stream)
+        torch.cuda.synchronize()
+        _barrier(world)
+        t_ar = _max_over_ranks(a_ev.elapsed_time(b_ev) / 10, world)
+        bus = 2 * n * 2 * (world - 1) / world / (t_ar * 1e-3) / 1e9
+        ar_alone = {"ms": t_ar, "bus_gbs": bus, "frac_of_900": bus / NVLINK_NOMINAL_GBS,
+                    "frac_of_measured_nvlink": bus / NVLINK_MEASURED_GBS,
+                    "launches": step.n_buckets * args.ar_pieces,
+                    "what": "smpu_allreduce_accumulator back to back (every bucket, the headline's ar_pieces)"}
     step.close()
     del step
 
@@ -988,6 +1010,8 @@ def main_ours(args):
         a = bus_gbs(kstat, args.steps, n, world, head_sharded)
         if a:
             a["impl"] = {1: "nccl", 2: "fused_lsa"}.get(ar_impl, str(ar_impl)) + ("_reduce_scatter" if head_sharded else "")
+            if ar_alone:
+                a["standalone"] = ar_alone
             out["allreduce"] = a
     if fused_variant:
         out["fused_final_variant"] = fused_variant
