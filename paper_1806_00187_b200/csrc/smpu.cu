@@ -110,6 +110,8 @@ struct smpu_ctx {
     size_t w16_off = 0;                                     // w16 inside the symmetric window
     std::vector<std::vector<std::pair<int64_t, int64_t>>> shard;   // per bucket: this rank's element ranges
     cudaStream_t comm_stream = nullptr, copy_stream = nullptr, dec_stream = nullptr, k2_stream = nullptr;
+    cudaStream_t k2_stream2 = nullptr;                      // second Adam stream (W > 1 pieces alternate)
+    cudaEvent_t k2_join = nullptr;
     std::vector<cudaEvent_t> ready;
     // all-reduce launches of bucket b: pieces[b] = element boundaries (one piece unless smpu_config.ar_pieces
     // pipelines them), ar_done[b][i] = piece i reduced
@@ -259,7 +261,8 @@ struct Timed {
             if (e) {
                 cudaEventRecord(e, s);
                 c->timed[kind].emplace_back(b, e);
-                int sid = s == c->comm_stream ? 1 : s == c->dec_stream ? 2 : s == c->k2_stream ? 3 : 0;
+                int sid = s == c->comm_stream ? 1 : s == c->dec_stream ? 2 :
+                          (s == c->k2_stream || s == c->k2_stream2) ? 3 : 0;
                 c->trace.push_back({kind, sid, b, e});
             }
         }
@@ -799,12 +802,16 @@ smpu_status launch_decision_lsa(smpu_ctx* ctx, cudaStream_t ds) {
 }
 
 // Adam per bucket on the ctx's K2 stream, each bucket behind its all-reduce and the decision (dec_ev)
+// Pieces alternate between two Adam streams: a piece whose all-reduce has landed need not wait for the previous
+// piece's Adam, which is still sharing HBM with the next all-reduce (the tail's HBM is not saturated: r2n timelines).
 smpu_status enqueue_adam(smpu_ctx* ctx) {
-    cudaStream_t ks = ctx->k2_stream;
-    CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
+    cudaStream_t ks2[2] = {ctx->k2_stream, ctx->k2_stream2};
+    for (cudaStream_t ks : ks2) CK(cudaStreamWaitEvent(ks, ctx->dec_ev, 0));
+    int j = 0;
     for (int b = 0; b < ctx->nb; ++b) {
         const auto& pc = ctx->pieces[b];
-        for (size_t i = 0; i + 1 < pc.size(); ++i) {   // each piece right behind its all-reduce
+        for (size_t i = 0; i + 1 < pc.size(); ++i, ++j) {   // each piece right behind its all-reduce
+            cudaStream_t ks = ks2[j & 1];
             CK(cudaStreamWaitEvent(ks, ctx->ar_done[b][i], 0));
             Timed t(ctx, SMPU_K2, ks);
             smpu_status st = ctx->sharded ? launch_k2_shard(ctx, b, DEC_APPLY, ks)
@@ -812,7 +819,9 @@ smpu_status enqueue_adam(smpu_ctx* ctx) {
             if (st != SMPU_OK) return st;
         }
     }
-    CK(cudaEventRecord(ctx->k2_done, ks));
+    CK(cudaEventRecord(ctx->k2_join, ctx->k2_stream2));
+    CK(cudaStreamWaitEvent(ctx->k2_stream, ctx->k2_join, 0));
+    CK(cudaEventRecord(ctx->k2_done, ctx->k2_stream));
     return SMPU_OK;
 }
 
@@ -1065,6 +1074,8 @@ void free_ctx(smpu_ctx* c) {
     if (c->tail_ev) cudaEventDestroy(c->tail_ev);
     if (c->dec_stream) cudaStreamDestroy(c->dec_stream);
     if (c->k2_stream) cudaStreamDestroy(c->k2_stream);
+    if (c->k2_stream2) cudaStreamDestroy(c->k2_stream2);
+    if (c->k2_join) cudaEventDestroy(c->k2_join);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (int j = 0; j < 2; ++j) {
         if (c->stage_free[j]) cudaEventDestroy(c->stage_free[j]);
@@ -1356,6 +1367,8 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
     IK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     IK(cudaStreamCreateWithPriority(&ctx->dec_stream, cudaStreamNonBlocking, hi_prio));
     IK(cudaStreamCreateWithFlags(&ctx->k2_stream, cudaStreamNonBlocking));
+    IK(cudaStreamCreateWithFlags(&ctx->k2_stream2, cudaStreamNonBlocking));
+    IK(cudaEventCreateWithFlags(&ctx->k2_join, cudaEventDisableTiming));
     for (int j = 0; j < 2; ++j) {
         IK(cudaEventCreateWithFlags(&ctx->stage_free[j], cudaEventDisableTiming));
         IK(cudaEventCreateWithFlags(&ctx->stage_full[j], cudaEventDisableTiming));
