@@ -56,10 +56,10 @@ def parse():
     ap.add_argument("--ar-ctas", type=int, default=0, help="smpu_config.ar_ctas (0: one per SM)")
     ap.add_argument("--ar-unroll", type=int, choices=[1, 2], default=1, help="smpu_config.ar_unroll")
     ap.add_argument("--ar-threads", type=int, choices=[256, 512], default=256, help="smpu_config.ar_threads")
-    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1, 2, 3], default=None,
+    ap.add_argument("--ar-copy-engine", type=int, choices=[0, 1, 2], default=None,
                     help="smpu_config.ar_copy_engine (replicated, W > 1): the bucket all-reduce's NVLink traffic by "
                          "the copy engines (cudaMemcpyAsync push + all-gather, SM fold only); 2: all buckets but the "
-                         "last; 3: every piece split, a quarter on the copy engines beside the SM kernel.  Default: 0 in m1 (the HBM-bound update step alone: the SM kernel moves the fewest "
+                         "last.  Default: 0 in m1 (the HBM-bound update step alone: the SM kernel moves the fewest "
                          "HBM bytes), 1 in m2 / train (a backward runs beside the exchange: keep its SMs)")
     ap.add_argument("--generator", choices=["real", "exact", "zero", "real_sparse"], default="real",
                     help="input family (SURVEY 8(d.2)); real_sparse = G_real with the row-sparse embedding gradient "

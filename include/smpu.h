@@ -111,9 +111,7 @@ typedef struct {
                                   peer for the reduce-scatter push and the all-gather, an SM kernel only for the local
                                   ascending-rank fold), so a bucket in flight holds no SM while a backward or K1 runs;
                                   2 = the copy engines for every bucket but the last, which is ready only once the
-                                  backward has ended and goes through the SM kernel (higher bandwidth); 3 = every
-                                  piece split, three quarters through the SM kernel and a quarter through the copy
-                                  engines at the same time (two streams).  Same bits.  The window grows by ~2 B per parameter of staging.  EINVAL with sharded,
+                                  backward has ended and goes through the SM kernel (higher bandwidth).  Same bits.  The window grows by ~2 B per parameter of staging.  EINVAL with sharded,
                                   ar_mcast or SMPU_AR_NCCL.  Collective: compared across ranks.                       */
 } smpu_config;
 

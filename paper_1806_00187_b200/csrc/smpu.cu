@@ -101,8 +101,6 @@ struct smpu_ctx {
     char* peer_win[kMaxLsaRanks] = {};
     cudaStream_t ce_stream[kMaxLsaRanks] = {};
     cudaEvent_t ce_fork = nullptr, ce_join[kMaxLsaRanks] = {};
-    cudaStream_t ce_comm = nullptr;                         // ar_copy_engine 3: the copy-engine leg's stream
-    cudaEvent_t ce_split_fork = nullptr, ce_split_join = nullptr;
     smpu_group* group = nullptr;                            // virtual rank of a one-GPU group (smpu_group_init)
     bool w16_in_win = false;                                // w16 is a slice of the window allocation
     cudaStream_t step_stream = nullptr;                     // group, sharded: the stream of the deferred tail
@@ -593,16 +591,7 @@ struct CeGeom {
 
 // ar_copy_engine 1: every bucket on the copy engines; 2: every bucket but the last (the last one is ready only when
 // the backward has ended, so nothing is left to overlap it with and k_ar32's higher in-situ bandwidth wins)
-bool ce_bucket(const smpu_ctx* ctx, int b) {
-    return ctx->ce && (ctx->cfg.ar_copy_engine == 1 || (ctx->cfg.ar_copy_engine == 2 && b + 1 < ctx->nb));
-}
-// ar_copy_engine 3: piece [lo, hi) is split at ce_split(lo, hi): [lo, mid) through the SM kernel, [mid, hi) through
-// the copy engines, concurrently on two streams (the copy-engine leg takes a quarter, on 16-element boundaries)
-int64_t ce_split(int64_t lo, int64_t hi) {
-    int64_t mid = (lo + (hi - lo) * 3 / 4) & ~(int64_t)15;
-    return mid < lo ? lo : mid;
-}
-bool ce_split_mode(const smpu_ctx* ctx) { return ctx->ce && ctx->cfg.ar_copy_engine == 3; }
+bool ce_bucket(const smpu_ctx* ctx, int b) { return ctx->ce && (ctx->cfg.ar_copy_engine == 1 || b + 1 < ctx->nb); }
 
 // Copies issued on the ctx's W - 1 copy streams forked from / joined into `cs`: copy j goes to `dst(j)` from
 // `src(j)`, `bytes(j)` bytes (skipped when 0).
@@ -623,8 +612,7 @@ smpu_status ce_copies(smpu_ctx* ctx, int count, cudaStream_t cs, F&& one) {
     return SMPU_OK;
 }
 
-smpu_status launch_ar_ce(smpu_ctx* ctx, int64_t lo, int64_t hi, size_t stage_off, cudaStream_t cs,
-                         uint32_t bar0 = 0, uint32_t bar1 = 1) {
+smpu_status launch_ar_ce(smpu_ctx* ctx, int64_t lo, int64_t hi, size_t stage_off, cudaStream_t cs) {
     const int W = ctx->world, r = ctx->rank;
     const CeGeom G(lo, hi, W);
     const LsaPeers pe = lsa_peers(ctx);
@@ -638,7 +626,7 @@ smpu_status launch_ar_ce(smpu_ctx* ctx, int64_t lo, int64_t hi, size_t stage_off
     });
     if (st != SMPU_OK) return st;
     // 2. every rank's pushes have landed; 3. fold my shard (+ rank 0: head / tail over peer memory)
-    k_ce_barrier<LsaPeers><<<1, 32, 0, cs>>>(pe, bar0);
+    k_ce_barrier<LsaPeers><<<1, 32, 0, cs>>>(pe, 0);
     CKL("k_ce_barrier");
 #define SMPU_CER(WW) k_ce_reduce<WW, LsaPeers><<<ctx->grid_ar, 256, 0, cs>>>(pe, lo, hi, stage_off)
     SMPU_BY_WORLD(W, SMPU_CER, "copy-engine all-reduce")
@@ -653,7 +641,7 @@ smpu_status launch_ar_ce(smpu_ctx* ctx, int64_t lo, int64_t hi, size_t stage_off
         bytes = (size_t)(G.uhi(r) - G.ulo(r)) * 32;
     });
     if (st != SMPU_OK) return st;
-    k_ce_barrier<LsaPeers><<<1, 32, 0, cs>>>(pe, bar1);
+    k_ce_barrier<LsaPeers><<<1, 32, 0, cs>>>(pe, 1);
     CKL("k_ce_barrier");
     ctx->launches[SMPU_ALLREDUCE] += 2;   // three kernels; the caller's Timed counted one
     return SMPU_OK;
@@ -723,20 +711,7 @@ smpu_status issue_ready_buckets(smpu_ctx* ctx) {
         for (size_t i = 0; i + 1 < pc.size(); ++i) {
             {
                 Timed t(ctx, SMPU_ALLREDUCE, cs);
-                if (ce_split_mode(ctx)) {
-                    // the copy-engine leg on its own stream with barrier indices of its own (the SM kernel's
-                    // CTAs use 0 .. grid_ar - 1 concurrently), joined before the piece counts as reduced
-                    const int64_t mid = ce_split(pc[i], pc[i + 1]);
-                    CK(cudaEventRecord(ctx->ce_split_fork, cs));
-                    CK(cudaStreamWaitEvent(ctx->ce_comm, ctx->ce_split_fork, 0));
-                    smpu_status st = launch_ar_ce(ctx, mid, pc[i + 1], ctx->ce_off[b][i], ctx->ce_comm,
-                                                  (uint32_t)ctx->grid_ar + 3, (uint32_t)ctx->grid_ar + 4);
-                    if (st != SMPU_OK) return st;
-                    st = launch_ar_fused(ctx, pc[i], mid, cs);
-                    if (st != SMPU_OK) return st;
-                    CK(cudaEventRecord(ctx->ce_split_join, ctx->ce_comm));
-                    CK(cudaStreamWaitEvent(cs, ctx->ce_split_join, 0));
-                } else if (ce_bucket(ctx, b)) {
+                if (ce_bucket(ctx, b)) {
                     smpu_status st = launch_ar_ce(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], cs);
                     if (st != SMPU_OK) return st;
                 } else if (ctx->ar_impl == SMPU_AR_FUSED) {
@@ -765,19 +740,6 @@ smpu_status group_issue_buckets(smpu_ctx* ctx) {
         for (smpu_ctx* q : g->m) CK(cudaStreamWaitEvent(g->comm, q->ready[b], 0));
         const auto& pc = ctx->pieces[b];
         for (size_t i = 0; i + 1 < pc.size(); ++i) {
-            if (ce_split_mode(ctx)) {
-                const int64_t mid = ce_split(pc[i], pc[i + 1]);
-                smpu_status st = launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world, pc[i],
-                                                mid, g->comm);
-                if (st != SMPU_OK) return st;
-                st = launch_ar_ce_group(ctx, mid, pc[i + 1], ctx->ce_off[b][i], g->comm);
-                if (st != SMPU_OK) return st;
-                for (smpu_ctx* q : g->m) {
-                    q->launches[SMPU_ALLREDUCE]++;
-                    CK(cudaEventRecord(q->ar_done[b][i], g->comm));
-                }
-                continue;
-            }
             smpu_status st = ce_bucket(ctx, b) ? launch_ar_ce_group(ctx, pc[i], pc[i + 1], ctx->ce_off[b][i], g->comm)
                                      : launch_ar_with(ctx, local_peers(g, g->per_rank, 0), g->per_rank * g->world,
                                                       pc[i], pc[i + 1], g->comm);
@@ -1069,7 +1031,7 @@ smpu_status check_cfg(const smpu_config* c) {
                                     "ar_unroll 1|2, ar_mcast 0|1, pdl 0|1, ar_pieces 1..64");
     if (c->ar_mcast && c->ar_vec_bytes != 32)
         return set_err(SMPU_EINVAL, "ar_mcast needs ar_vec_bytes = 32");
-    if (c->ar_copy_engine < 0 || c->ar_copy_engine > 3) return set_err(SMPU_EINVAL, "ar_copy_engine must be 0..3");
+    if (c->ar_copy_engine < 0 || c->ar_copy_engine > 2) return set_err(SMPU_EINVAL, "ar_copy_engine must be 0|1|2");
     if (c->ar_copy_engine && (c->sharded || c->ar_mcast || c->allreduce == SMPU_AR_NCCL))
         return set_err(SMPU_EINVAL, "ar_copy_engine runs the replicated fused all-reduce only (not with sharded, "
                                     "ar_mcast or SMPU_AR_NCCL)");
@@ -1125,9 +1087,6 @@ void free_ctx(smpu_ctx* c) {
     for (auto& x : c->ce_stream) if (x) cudaStreamDestroy(x);
     for (auto& e : c->ce_join) if (e) cudaEventDestroy(e);
     if (c->ce_fork) cudaEventDestroy(c->ce_fork);
-    if (c->ce_comm) cudaStreamDestroy(c->ce_comm);
-    if (c->ce_split_fork) cudaEventDestroy(c->ce_split_fork);
-    if (c->ce_split_join) cudaEventDestroy(c->ce_split_join);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     cudaFree(c->tok_dev);
@@ -1357,8 +1316,7 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         for (int b = 0; b < ctx->nb; ++b) {
             const auto& pc = ctx->pieces[b];
             for (size_t i = 0; i + 1 < pc.size(); ++i) {
-                const int64_t lo_ce = cfg->ar_copy_engine == 3 ? ce_split(pc[i], pc[i + 1]) : pc[i];
-                const int64_t v0 = (lo_ce + 15) & ~(int64_t)15, v1 = pc[i + 1] & ~(int64_t)15;
+                const int64_t v0 = (pc[i] + 15) & ~(int64_t)15, v1 = pc[i + 1] & ~(int64_t)15;
                 const int64_t units = v1 > v0 ? (v1 - v0) / 16 : 0, per = (units + world - 1) / world;
                 ctx->ce_off[b].push_back(win_bytes);
                 win_bytes += ((size_t)world * per * 32 + 255) & ~(size_t)255;
@@ -1506,7 +1464,7 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
             memset(&reqs, 0, sizeof reqs);
             // one per all-reduce CTA (indices 0 / 1 also serve the copy-engine all-reduce's barrier kernels) +
             // early decision + late decision + end-of-update (sharded)
-            reqs.lsaBarrierCount = ctx->grid_ar + 5;   // + 3 / + 4: the split copy-engine leg's barriers
+            reqs.lsaBarrierCount = ctx->grid_ar + 3;
             reqs.lsaMultimem = cfg->ar_mcast != 0;
             ncclResult_t r = ncclDevCommCreate(ctx->comm, &reqs, &ctx->devcomm);
             ctx->have_devcomm = r == ncclSuccess;
@@ -1543,9 +1501,6 @@ static smpu_status create_ctx(smpu_ctx** out, const smpu_config* cfg, int world,
         }
     }
     if (ctx->ce) {
-        IK(cudaStreamCreateWithPriority(&ctx->ce_comm, cudaStreamNonBlocking, hi_prio));
-        IK(cudaEventCreateWithFlags(&ctx->ce_split_fork, cudaEventDisableTiming));
-        IK(cudaEventCreateWithFlags(&ctx->ce_split_join, cudaEventDisableTiming));
         IK(cudaEventCreateWithFlags(&ctx->ce_fork, cudaEventDisableTiming));
         for (int j = 0; j + 1 < world; ++j) {
             IK(cudaStreamCreateWithPriority(&ctx->ce_stream[j], cudaStreamNonBlocking, hi_prio));

@@ -41,7 +41,7 @@ def draw_case(rng, W):
                 d.update(r=int(rng.integers(0, W)))
             inj.append(d)
     sharded = bool(rng.integers(0, 4) == 0)
-    ce = 0 if sharded else int(rng.integers(0, 4))
+    ce = 0 if sharded else int(rng.integers(0, 3))
     pieces = 1 if sharded else int(rng.integers(1, 4))
     bucket_bytes = [2, 1000, 16_384, 100_000, 1 << 20][int(rng.integers(0, 5))]
     return tensors, c, inj, sharded, ce, pieces, bucket_bytes

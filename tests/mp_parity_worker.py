@@ -58,16 +58,16 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     # bucket threshold chosen so buckets split the vector at unaligned boundaries
     ar = {"auto": P.smpu.AR_AUTO, "nccl": P.smpu.AR_NCCL, "fused": P.smpu.AR_FUSED, "ce": P.smpu.AR_FUSED,
-          "ce2": P.smpu.AR_FUSED, "ce3": P.smpu.AR_FUSED}[impl]
+          "ce2": P.smpu.AR_FUSED}[impl]
     ocfg = O.Config(accum_fp32=acc32)
     step = P.UpdateStep(wl.numel, theta0 if rank == 0 else np.zeros_like(theta0),
                         lib_cfg(wl, ocfg, bucket_bytes=400_000, allreduce=ar, split_tensors=int(split),
-                                ar_copy_engine={"ce": 1, "ce2": 2, "ce3": 3}.get(impl, 0)), world=world,
+                                ar_copy_engine={"ce": 1, "ce2": 2}.get(impl, 0)), world=world,
                         rank=rank,
                         nccl_id=obj[0], device=local)
     assert step.n_buckets >= 2
     fused = step.allreduce_impl == P.smpu.AR_FUSED
-    if impl in ("fused", "ce", "ce2", "ce3"):
+    if impl in ("fused", "ce", "ce2"):
         assert fused
     shard_step = None
     if sharded:   # the SURVEY f2 variant beside the replicated ctx, same inputs: must agree bitwise on its shard

@@ -198,7 +198,7 @@ def test_config_and_group_argument_errors_need_no_gpu(P):
     wl = models.Workload("args", [("w", 1000, 0)], 1, 1)
     theta0 = np.zeros(1000, np.float32)
     for bad in (dict(ar_threads=300), dict(ar_vec_bytes=8), dict(ar_unroll=3), dict(ar_ctas=-1), dict(pdl=2),
-                dict(ar_mcast=1, ar_vec_bytes=16), dict(ar_copy_engine=4), dict(ar_copy_engine=1, sharded=1),
+                dict(ar_mcast=1, ar_vec_bytes=16), dict(ar_copy_engine=3), dict(ar_copy_engine=1, sharded=1),
                 dict(ar_copy_engine=1, ar_mcast=1), dict(ar_copy_engine=1, allreduce=P.smpu.AR_NCCL)):
         with pytest.raises(P.SmpuError) as ei:
             P.UpdateStep(wl.numel, theta0, P.config_default(**bad))

@@ -161,13 +161,12 @@ def test_virtual_pieces(world, split):
 
 @pytest.mark.parametrize("world,mode,split,ce", [(2, "calls", 1, 1), (3, "buckets", 1, 1), (4, "calls", 3, 1),
                                                  (8, "buckets", 1, 1), (5, "many", 2, 1), (4, "buckets", 1, 2),
-                                                 (8, "calls", 2, 2), (2, "calls", 1, 3), (6, "buckets", 2, 3)])
+                                                 (8, "calls", 2, 2)])
 def test_virtual_copy_engine(world, mode, split, ce):
     """smpu_config.ar_copy_engine: the bucket all-reduce's traffic moved by cudaMemcpyAsync (push of every shard to
     its owner's staging, fold, all-gather of R): decisions and R bitwise the oracle's (the fold is k_ar32's
     ascending-rank order), alone and with ar_pieces, through every injection kind; ce = 2: every bucket but the last
-    on the copy engines, the last through k_ar32 (the two share the LSA barriers); ce = 3: every piece split between
-    k_ar32 and the copy engines (disjoint ranges)."""
+    on the copy engines, the last through k_ar32 (the two share the LSA barriers)."""
     _run(world, "real", False, mode=mode, ar_copy_engine=ce, ar_pieces=split)
 
 
