@@ -52,7 +52,7 @@ def test_random_cases_on_real_peers(world):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29601 + world), "tests/mp_fuzz_worker.py",
+           "--master-addr", "127.0.0.1", "--master-port", str(29701 + world), "tests/mp_fuzz_worker.py",
            os.environ.get("SMPU_FUZZ_EXAMPLES", "16" if world == 2 else "10"),
            os.environ.get("SMPU_FUZZ_SEED", str(31 + world))]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=3000)
