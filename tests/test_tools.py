@@ -1,0 +1,25 @@
+"""The measurement tools regenerate their committed summaries from committed records (CPU only)."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_c4_summary_from_committed_sweeps(tmp_path):
+    out = tmp_path / "c4.txt"
+    files = [os.path.join(ROOT, "profiles", "r2", d, f) for d, f in
+             (("f_w4", "c4_w4.jsonl"), ("dd_w4", "c4_w2.jsonl"))]
+    subprocess.run([sys.executable, "tools/c4_summary.py", str(out)] + files, cwd=ROOT, check=True,
+                   capture_output=True)
+    txt = out.read_text()
+    assert "## W = 4, update_freq = 16" in txt and "## W = 2, update_freq = 1" in txt
+    # every C4 threshold of SURVEY 8(d.1) is in the W = 4 sweep
+    w4 = txt.split("## W = 4, update_freq = 16")[1].split("##")[0]
+    assert [int(l.split()[0]) for l in w4.strip().splitlines()[1:]] == [1, 2, 4, 8, 16, 32, 64, 128, 150, 256]
+
+
+def test_overlap_model_reproduces_committed_table(tmp_path):
+    out = tmp_path / "overlap.txt"
+    subprocess.run([sys.executable, "tools/overlap_predict.py", str(out)], cwd=ROOT, check=True, capture_output=True)
+    assert out.read_text() == open(os.path.join(ROOT, "profiles", "r2_overlap_model.txt")).read()
