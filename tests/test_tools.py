@@ -20,6 +20,8 @@ def test_c4_summary_from_committed_sweeps(tmp_path):
 
 
 def test_overlap_model_reproduces_committed_table(tmp_path):
+    if not os.path.exists(os.path.join(ROOT, "paper_1806_00187_b200", "libsmpu_sched.so")):
+        subprocess.run([sys.executable, os.path.join("paper_1806_00187_b200", "_build.py")], cwd=ROOT, check=True)
     out = tmp_path / "overlap.txt"
     subprocess.run([sys.executable, "tools/overlap_predict.py", str(out)], cwd=ROOT, check=True, capture_output=True)
     assert out.read_text() == open(os.path.join(ROOT, "profiles", "r2_overlap_model.txt")).read()
