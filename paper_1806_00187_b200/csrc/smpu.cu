@@ -14,8 +14,8 @@
 // paper's "background thread", becomes a stream: enqueue is already asynchronous); once the last
 // micro-batch is accumulated, a decision stream exchanges 16 bytes per rank (N_r and max|A_r|: through peer
 // memory in one kernel, or an NCCL all-reduce on a second communicator) and K0 EARLY decides overflow exactly
-// in the common case; a K2 stream then runs Adam on bucket b as soon as bucket b's all-reduce lands,
-// overlapping the remaining all-reduces.  smpu_step enqueues only the (normally empty) fallback.  W = 1:
+// in the common case; two K2 streams (pieces alternate) then run Adam on each all-reduce piece as soon as it
+// lands, overlapping the remaining all-reduces.  smpu_step enqueues only the (normally empty) fallback.  W = 1:
 // K1 -> K0 -> K2 on the caller's streams.  No host synchronisation anywhere on the update path.
 #include <cuda_runtime.h>
 #include <nccl.h>
