@@ -25,3 +25,18 @@ def test_overlap_model_reproduces_committed_table(tmp_path):
     out = tmp_path / "overlap.txt"
     subprocess.run([sys.executable, "tools/overlap_predict.py", str(out)], cwd=ROOT, check=True, capture_output=True)
     assert out.read_text() == open(os.path.join(ROOT, "profiles", "r2_overlap_model.txt")).read()
+
+
+def test_trace_tail_on_a_synthetic_timeline(tmp_path):
+    """tools/trace_tail.py: the last update starts at its k1_first; times relative to the end of its last K1."""
+    import json
+    ev = [("k1_first", "caller", 0.0, 0.1), ("k1_add", "caller", 0.1, 0.3), ("k2_adam", "adam_per_bucket", 0.3, 0.9),
+          ("k1_first", "caller", 1.0, 1.1), ("k1_add", "caller", 1.1, 1.3), ("allreduce", "allreduce", 1.2, 1.6),
+          ("k2_adam", "adam_per_bucket", 1.6, 2.0)]
+    p = tmp_path / "t.jsonl"
+    p.write_text("".join(json.dumps({"rank": 0, "kernel": k, "stream": s, "start_ms": a, "end_ms": b}) + "\n"
+                         for k, s, a, b in ev))
+    out = subprocess.run([sys.executable, "tools/trace_tail.py", str(p)], cwd=ROOT, check=True, capture_output=True,
+                         text=True).stdout
+    assert "update 1.000 ms, tail after the last K1 0.700 ms" in out
+    assert "'allreduce': 0.3" in out and "'adam_per_bucket': 0.4" in out
